@@ -1,0 +1,284 @@
+#!/usr/bin/env python
+"""Benchmark of the PolyMage-GPU hot path on B200 (BASELINE.json metric: output Mpixels/s and % of the HBM
+roofline).
+
+Workload (BASELINE.json configs[1], fits one GPU): Harris corner detection, 11 stages, 6400x6400 f32,
+seeded U[0,1) synthetic image (pmg_inputs.py, seed 1002).  One step = one full pipeline run (every kernel
+of the plan).  Inputs are larger than L2 (164 MB in + 164 MB out vs 126 MB L2) and two buffer sets are
+rotated between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload harris] [--impl reference]
+
+N > 1 (torchrun, one process per GPU): the image is split into row bands (pmg_run_band); each rank
+computes its band with the pipeline-wide halo recomputed locally, no collective on the data path; time =
+max over ranks of the device time; value = whole-image pixels / that time ("scaling": "strong").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+import pmg_inputs as PI  # noqa: E402
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[1]) for s in self.samples if len(s) > 2 and s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if len(s) > 2 and s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline(wl, max_rows=None):
+    """The oracle as it stands, on a bounded row band of the same workload, on this host's cores."""
+    sys.path.insert(0, str(ROOT))
+    from oracle import evaluate
+    W, H = wl.params["W"], wl.params["H"]
+    rows = max_rows or max(8, H // 16)
+    sub = PI.Workload(wl.name, wl.pipeline, {"W": W, "H": rows}, wl.seed)
+    inp = sub.inputs()
+    t0 = time.perf_counter()
+    evaluate(sub.text, sub.params, inp)
+    dt = time.perf_counter() - t0
+    return {"value": W * rows / dt / 1e6, "unit": "Mpixels/s", "cores": 1, "kind": "oracle",
+            "sample": f"{wl.name} band of {rows} of {H} rows x {W} cols (numpy, single thread), {dt:.2f} s"}
+
+
+def reference_arm(args, wl):
+    """--impl reference: the independent oracle timed on the host (no reference package exists)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W, H = wl.params["W"], wl.params["H"]
+    rows = max(8, H // 64)
+    sub = PI.Workload(wl.name, wl.pipeline, {"W": W, "H": rows}, wl.seed)
+    inp = sub.inputs()
+    from oracle import evaluate
+    for _ in range(args.warmup):
+        evaluate(sub.text, sub.params, inp)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        evaluate(sub.text, sub.params, inp)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = W * rows / dt / 1e6
+    print(json.dumps({
+        "impl": "reference", "metric": "output Mpixels/s (" + wl.name + ")", "value": v, "unit": "Mpixels/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.note, "sample_rows": rows},
+        "cpu_baseline": {"value": v, "unit": "Mpixels/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{rows} x {W} band per step (numpy, single thread)"},
+        "e2e": {"value": v, "unit": "Mpixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="harris", choices=sorted(PI.WORKLOADS))
+    ap.add_argument("--impl", default="pmg", choices=["pmg", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opts", default="", help="manual schedule, e.g. vec=4,chunks=1,rows=32,warps=4,prefetch=4")
+    args = ap.parse_args()
+    wl = PI.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_07190_b200 as pmg
+    from paper_1909_07190_b200.pipeline import _buf  # noqa: F401
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = local
+    torch.cuda.set_device(dev)
+    torch.cuda.init()
+    stream = torch.cuda.current_stream(dev)
+
+    opts = None
+    if args.opts:
+        kv = dict(x.split("=") for x in args.opts.split(","))
+        opts = pmg.sched_opts(**{k: int(v) for k, v in kv.items()})
+    pipe = pmg.Pipeline(wl.text)
+    plan = pmg.Plan(pipe, wl.params, device=dev, opts=opts)
+    desc = plan.describe()
+    W, H = wl.params["W"], wl.params["H"]
+    inputs_np = wl.inputs()
+
+    from gpu_util_bench import device_inputs
+    nb = world
+    band = rank
+    o_r0, o_r1, i_r0, i_r1 = plan.band_rows(band, nb)
+    sets = 2
+    in_sets, out_sets = [], []
+    for _ in range(sets):
+        ins = device_inputs(plan, inputs_np, dev, rows=(i_r0, i_r1) if nb > 1 else None)
+        outs = [pmg.empty_pitched((*o.shape[:-2], o_r1 - o_r0, o.shape[-1]), o.dtype, f"cuda:{dev}") for o in plan.outputs]
+        in_sets.append(ins)
+        out_sets.append(outs)
+    ws = plan.workspace()
+
+    def step(i):
+        ins, outs = in_sets[i % sets], out_sets[i % sets]
+        if nb > 1:
+            plan.run_band(band, nb, ins, outs, ws, stream)
+        else:
+            plan.run(ins, outs, ws, stream)
+
+    for i in range(max(3, args.warmup)):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    # dominant kernel: per-launch CUDA-event timing on the launching stream (single-kernel plans: the step)
+    nk = plan.num_kernels
+    bytes_in = sum(int(np.prod(io.shape)) * pmg._binding.DTYPE_SIZE[io.dtype] for io in plan.inputs)
+    bytes_out = sum(int(np.prod(io.shape)) * pmg._binding.DTYPE_SIZE[io.dtype] for io in plan.outputs)
+    algo_bytes = (bytes_in + bytes_out) / nb
+    pk, pk_kind = peaks()
+    peak = float(pk["hbm_gbs"])
+    achieved = algo_bytes / (ms * 1e-3) / 1e9
+    value = W * H / (ms * 1e-3) / 1e6
+
+    # end-to-end through the public API with host buffers: pinned H2D of the inputs + run + D2H of the output
+    e2e = None
+    if nb == 1:
+        host_in = [torch.from_numpy(np.ascontiguousarray(inputs_np[io.name]).view(
+            {np.dtype(np.uint16): np.int16}.get(inputs_np[io.name].dtype, inputs_np[io.name].dtype))).pin_memory()
+            for io in plan.inputs]
+        host_out = [torch.empty(o.shape, dtype=pmg.pipeline._torch_dtype(o.dtype)).pin_memory() for o in plan.outputs]
+        ins, outs = in_sets[0], out_sets[0]
+
+        def e2e_step():
+            for h, d in zip(host_in, ins):
+                d.view(h.dtype).copy_(h, non_blocking=True)
+            plan.run(ins, outs, ws, stream)
+            for h, d in zip(host_out, outs):
+                h.copy_(d, non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n_e2e = max(3, args.steps // 4)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / n_e2e
+        e2e = {"value": W * H / (ems * 1e-3) / 1e6, "unit": "Mpixels/s", "h2d_bytes_per_step": bytes_in,
+               "d2h_bytes_per_step": bytes_out, "ms_per_step": ems}
+
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.workload}_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": f"output Mpixels/s ({wl.name}); % of HBM roofline", "value": value, "unit": "Mpixels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded U[0,1) image, pmg_inputs.py)",
+        "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
+                   "l2": "inputs+outputs (328 MB) larger than L2 (126 MB); 2 rotating buffer sets",
+                   "schedule": [g["config"] for g in desc["schedule"]["groups"]],
+                   "kernels": desc["kernels"]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": pk_kind,
+                     "note": "algorithmic bytes = compulsory input + output bytes per launch; "
+                             f"{nk} kernel(s) per step, timed per step on the launching stream"},
+        "gpu_launches": nk * args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

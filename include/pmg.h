@@ -1,0 +1,191 @@
+/*
+ * pmg.h — C ABI of the B200-native PolyMage-GPU hot path (warp-overlapped + hybrid tiling).
+ *
+ * The calls follow the paper's statement of the problem (§2.2): a pipeline is a
+ * DAG of stages over integer domains parameterised by the image extents ("the number of rows and
+ * columns", lines 286-287); its liveouts are the outputs (line 302); kernels take image sizes as
+ * runtime parameters (§5); all data resides on the GPU (§7).
+ *
+ *   pmg_pipeline_parse   text -> validated stage DAG                (§2.2; grammar extends SPEC.md l.81)
+ *   pmg_schedule         host-only: fusion groups + tile/block/fracReg/txSz with the Alg. 2 cost
+ *                        (§6), JSON report; no GPU needed
+ *   pmg_plan_create      schedule + emit + compile (NVRTC, sm_100a) one OTPW/hybrid kernel per group
+ *   pmg_run / pmg_run_band / pmg_run_batch   stream-ordered launches on caller-owned device buffers
+ *
+ * Layout: every image / stage buffer is planar [c][y][x], x fastest.  A buffer is described by
+ * pmg_buf{ptr, row_pitch_bytes, plane_pitch_bytes}.  Device pointers and pitches passed to run calls
+ * must be multiples of 16 bytes (TMA bulk-copy / 128-bit vector I/O); tables (LUTs) may have any
+ * alignment.  Element types are the pipeline's declared dtypes.
+ *
+ * Ownership: the library owns pipeline / plan handles (create/destroy pairs; destroy is NULL-safe).
+ * The caller owns every device buffer, the workspace and the stream.  Run calls are asynchronous and
+ * stream-ordered: no allocation, no host synchronisation, no device switch (the plan's device must be
+ * current — otherwise PMG_ERR_ARG).
+ *
+ * Errors: every call returns pmg_status; pmg_last_error() gives a thread-local message for the last
+ * non-OK status on the calling thread (parse errors carry "line:col").  Launch-configuration errors
+ * return PMG_ERR_CUDA immediately; asynchronous device faults surface at the caller's next sync.
+ * PMG_ERR_INFEASIBLE: every candidate schedule has infinite cost (Alg. 2, 945, 961).
+ *
+ * Concurrency: a pipeline is immutable and shareable across threads; a plan may run concurrently on
+ * different streams only with distinct workspaces.  Outputs are bit-identical for any schedule, band
+ * split or batch split (DESIGN.md §"Determinism").  No NCCL here: process groups and gathers belong to
+ * the caller (PyTorch).
+ */
+#ifndef PMG_H
+#define PMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PMG_OK = 0,
+  PMG_ERR_PARSE = -1,       /* syntax error, undeclared reference, cyclic reference, bad index form */
+  PMG_ERR_INVALID = -2,     /* invalid handle / semantic error */
+  PMG_ERR_UNSUPPORTED = -3, /* valid pipeline the kernel generator cannot run */
+  PMG_ERR_INFEASIBLE = -4,  /* all schedules cost infinity */
+  PMG_ERR_SHAPE = -5,       /* parameter values give an empty / inconsistent domain */
+  PMG_ERR_CUDA = -6,        /* CUDA driver error (or no driver) */
+  PMG_ERR_NVRTC = -7,       /* runtime compilation failed */
+  PMG_ERR_OOM = -8,
+  PMG_ERR_ARG = -9          /* bad argument: NULL, misaligned buffer, wrong device, buffer count */
+} pmg_status;
+
+typedef enum { PMG_U8 = 1, PMG_U16 = 2, PMG_I16 = 3, PMG_I32 = 4, PMG_F32 = 5 } pmg_dtype;
+
+typedef struct pmg_pipeline_s* pmg_pipeline; /* immutable after parse */
+typedef struct pmg_plan_s* pmg_plan;         /* bound to (pipeline, params, device, schedule) */
+
+/* one input image / table / output liveout: extents outermost first ([c][y][x]); ndim 1..3 */
+typedef struct {
+  char name[64];
+  int32_t dtype;       /* pmg_dtype */
+  int32_t ndim;
+  int32_t is_table;    /* inputs only: 1 for a 1-D lookup table */
+  int32_t reserved;
+  int64_t extent[3];
+} pmg_io_desc;
+
+/* device buffer: planar [c][y][x]; pitches in bytes (plane pitch ignored for <3-D tensors) */
+typedef struct {
+  void* ptr;
+  int64_t row_pitch_bytes;
+  int64_t plane_pitch_bytes;
+} pmg_buf;
+
+/* GPU description: Table 1 of the paper plus B200 additions */
+typedef struct {
+  char name[32];
+  int32_t nsms;               /* NSMs */
+  int32_t cores_per_sm;       /* CoresPerSM (FP32 lanes) */
+  int32_t max_warps_per_sm;   /* MaxWarpPerSM */
+  int32_t max_tb_per_sm;      /* MaxTbPerSM */
+  int32_t regs_per_sm;        /* RegPerSM */
+  int32_t max_regs_per_thread;/* MaxRegPerTh */
+  int32_t max_threads_per_sm; /* MaxThPerSM (used by Alg. 2 l.963, absent from Table 1) */
+  int32_t warp_size;          /* WarpSize */
+  int64_t shmem_per_sm;       /* ShMemPerSM, bytes */
+  int64_t max_shmem_per_tb;   /* MaxShMemPerTb, bytes */
+  double gl_mem_bw;           /* GlMemBW, bytes/s */
+  int32_t gl_tx_size[2];      /* GlMemTxSz choices: 32 (L2 sector) and 128 (L1 line) */
+  int64_t l2_bytes;           /* B200 addition */
+  double sm_clock_hz;         /* B200 addition (compute-time model) */
+} pmg_gpu_spec;
+
+/* cost weights w1..w7 (Table 3) */
+typedef struct {
+  double w[7];
+} pmg_weights;
+
+/* schedule overrides (SPEC.md l.631 flags); -1 / NULL = automatic */
+typedef struct {
+  const int32_t* group_of_stage; /* NULL = DP fusion; else group index per stage (declaration order) */
+  int32_t vec;          /* V: consecutive x points per lane per chunk (1, 2, 4) */
+  int32_t chunks;       /* TX: parallelogram (chunk) tiles per warp tile along x */
+  int32_t smem_chunks;  /* S: chunks kept in shared memory; chunks-S in registers (fracReg = (TX-S)/TX) */
+  int32_t rows;         /* TH: rows per warp tile (tile size in y) */
+  int32_t warps;        /* warps per thread block (TB size / 32) */
+  int32_t prefetch;     /* input rows in flight per warp (TMA ring depth) */
+  int32_t tx_size;      /* 32 or 128 */
+  int32_t budget;       /* max candidates per group (bounded search); <=0 = exhaustive */
+  int32_t fuse;         /* 0 = one stage per group, 1 = DP fusion (default) */
+  int32_t reserved[7];
+} pmg_sched_opts;
+
+const char* pmg_last_error(void);
+const char* pmg_version(void);
+
+/* ---- pipeline (host only) ---- */
+pmg_status pmg_pipeline_parse(const char* text, size_t len, pmg_pipeline* out);
+void pmg_pipeline_destroy(pmg_pipeline p); /* NULL-safe */
+int pmg_pipeline_num_params(pmg_pipeline p);
+pmg_status pmg_pipeline_param_name(pmg_pipeline p, int idx, char* buf, size_t cap);
+int pmg_pipeline_num_stages(pmg_pipeline p);
+pmg_status pmg_pipeline_stage_name(pmg_pipeline p, int idx, char* buf, size_t cap);
+/* inputs: images then tables, declaration order; outputs: liveouts in declaration order */
+int pmg_pipeline_num_io(pmg_pipeline p, int is_output);
+pmg_status pmg_pipeline_io(pmg_pipeline p, int is_output, int idx, const int64_t* params, int nparams,
+                           pmg_io_desc* out);
+/* dependence / footprint table as JSON (§2.3; per edge and dim: offsets, scale) */
+pmg_status pmg_pipeline_describe(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap,
+                                 size_t* needed);
+
+/* ---- GPU description and weights ---- */
+pmg_status pmg_gpu_spec_preset(const char* name /* "gtx1080ti", "teslav100", "b200" */, pmg_gpu_spec* out);
+pmg_status pmg_gpu_spec_query(int device, double measured_bw_gbs /* <=0: preset value */, pmg_gpu_spec* out);
+pmg_status pmg_weights_preset(const char* name /* "gtx1080ti", "teslav100", "b200" */, pmg_weights* out);
+void pmg_sched_opts_default(pmg_sched_opts* o);
+
+/* ---- host-only analysis (no GPU) ----
+ * pmg_schedule: fusion grouping + per-group configuration with every Alg. 2 term, as JSON.
+ * pmg_analyze_group: the paper's §4 geometry and Alg. 2 for one explicit group and configuration
+ * (paper notation: tile T, block B, fracReg, txSz); used to pin the worked examples of §3/§4.        */
+pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                        const pmg_weights* w, const pmg_sched_opts* opts, char* json, size_t cap, size_t* needed);
+pmg_status pmg_analyze_group(pmg_pipeline p, const int64_t* params, int nparams, const char* stages_csv,
+                             const int32_t tile[3], const int32_t block[3], double frac_reg, int32_t tx_size,
+                             int32_t regs_per_stage, const pmg_gpu_spec* spec, const pmg_weights* w,
+                             char* json, size_t cap, size_t* needed);
+/* emit the CUDA source of every group kernel (no compilation); JSON {"groups":[{"name","source"}]} */
+pmg_status pmg_emit(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                    const pmg_weights* w, const pmg_sched_opts* opts, char* json, size_t cap, size_t* needed);
+/* compile every group kernel for sm_100a with NVRTC (no GPU needed); writes cubins + sources under dir */
+pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                          const pmg_weights* w, const pmg_sched_opts* opts, const char* out_dir,
+                          char* json, size_t cap, size_t* needed);
+
+/* ---- plans (GPU) ---- */
+pmg_status pmg_plan_create(pmg_pipeline p, const int64_t* params, int nparams, int device,
+                           const pmg_gpu_spec* spec /* NULL = query device */, const pmg_weights* w /* NULL = b200 */,
+                           const pmg_sched_opts* opts /* NULL = automatic */, pmg_plan* out);
+void pmg_plan_destroy(pmg_plan plan); /* NULL-safe; caller ensures no run is in flight */
+pmg_status pmg_plan_describe(pmg_plan plan, char* buf, size_t cap, size_t* needed); /* JSON */
+pmg_status pmg_plan_workspace_bytes(pmg_plan plan, size_t* out);
+int pmg_plan_num_kernels(pmg_plan plan);
+
+/* full-image run: in[] = images then tables (declaration order), out[] = liveouts */
+pmg_status pmg_run(pmg_plan plan, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace,
+                   void* stream /* cudaStream_t / CUstream; NULL = legacy default stream */);
+/* nframes independent images: frame f of tensor i is at in[i].ptr + f * frame_stride_bytes[i] */
+pmg_status pmg_run_batch(pmg_plan plan, int nframes, const pmg_buf* in, const int64_t* in_frame_stride, int nin,
+                         const pmg_buf* out, const int64_t* out_frame_stride, int nout, void* workspace, void* stream);
+/* row bands (multi-GPU sharding): band b of n computes output rows [out_r0, out_r1) of every
+ * liveout; it needs input image rows [in_r0, in_r1) (pipeline-wide cumulative halo, clipped).  Rows are
+ * of the pipeline's full-resolution row space (parameter H). */
+pmg_status pmg_band_rows(pmg_plan plan, int band, int nbands, int64_t* out_r0, int64_t* out_r1, int64_t* in_r0,
+                         int64_t* in_r1);
+/* in[i] points at global row in_r0 of image i (tables: whole table); out[j] at global row out_r0 */
+pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, int nin, const pmg_buf* out,
+                        int nout, void* workspace, void* stream);
+
+/* device self-test of the warp-shuffle semantics of Fig. 1: lane 0 receives the sum */
+pmg_status pmg_selftest_shuffle(int device, int32_t* lane0_sum);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMG_H */

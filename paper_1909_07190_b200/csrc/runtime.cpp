@@ -1,0 +1,406 @@
+// runtime.cpp — NVRTC compilation for sm_100a, plan creation, workspace layout, band geometry and the
+// stream-ordered launch of one kernel per fused group (§6.2: "the sum of
+// execution time of all generated CUDA kernels").
+#include "runtime.hpp"
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <regex>
+#include <sstream>
+
+#include "cudrv.hpp"
+
+namespace pmg {
+
+#include "kernels_embed.inc"   // kOtpwHeader: kernels/pmg_otpw.cuh as a string (generated at build time)
+
+static uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ULL) {
+  for (unsigned char c : s) { h ^= c; h *= 1099511628211ULL; }
+  return h;
+}
+
+std::string kernel_dir() {
+  Dl_info info;
+  if (dladdr((void*)&kernel_dir, &info) && info.dli_fname) {
+    std::string f = info.dli_fname;
+    auto pos = f.rfind('/');
+    if (pos != std::string::npos) return f.substr(0, pos);
+  }
+  return ".";
+}
+
+static std::string cache_dir() {
+  const char* e = getenv("PMG_CACHE_DIR");
+  std::string d = e && *e ? e : kernel_dir() + "/../build/cubin_cache";
+  std::string acc;
+  std::stringstream ss(d);
+  std::string part;
+  if (!d.empty() && d[0] == '/') acc = "";
+  while (std::getline(ss, part, '/')) {
+    if (part.empty()) { acc += "/"; continue; }
+    acc += part;
+    mkdir(acc.c_str(), 0755);
+    acc += "/";
+  }
+  return d;
+}
+
+static const char* kOptions[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
+                                 "--ptxas-options=-v", "-default-device", "-DPMG_NVRTC=1"};
+
+static void parse_ptxas(Compiled& c) {
+  std::smatch m;
+  if (std::regex_search(c.log, m, std::regex("Used ([0-9]+) registers"))) c.regs = std::stoi(m[1]);
+  if (std::regex_search(c.log, m, std::regex("([0-9]+) bytes spill stores, ([0-9]+) bytes spill loads"))) {
+    c.spill_stores = std::stoi(m[1]);
+    c.spill_loads = std::stoi(m[2]);
+  }
+  if (std::regex_search(c.log, m, std::regex("([0-9]+) bytes smem"))) c.smem_static = std::stoi(m[1]);
+}
+
+Compiled jit_compile(const std::string& name, const std::string& source) {
+  Compiled c;
+  c.name = name;
+  c.source = source;
+  int maj = 0, min = 0;
+  nvrtcVersion(&maj, &min);
+  std::string key_src = source + "\n//" + std::string(kOtpwHeader);
+  for (const char* o : kOptions) key_src += std::string(" ") + o;
+  key_src += " nvrtc" + std::to_string(maj) + "." + std::to_string(min);
+  char hex[32];
+  snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(key_src));
+  std::string dir = cache_dir();
+  std::string base = dir + "/" + name + "_" + hex;
+  {
+    std::ifstream f(base + ".cubin", std::ios::binary);
+    std::ifstream lg(base + ".log");
+    if (f && lg) {
+      c.cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+      c.log.assign(std::istreambuf_iterator<char>(lg), std::istreambuf_iterator<char>());
+      if (!c.cubin.empty()) {
+        c.from_cache = true;
+        parse_ptxas(c);
+        return c;
+      }
+    }
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  // keep the generated source on disk so ncu --import-source / -lineinfo map back to it
+  std::string src_path = base + ".cu";
+  { std::ofstream f(src_path); f << source; }
+  nvrtcProgram prog;
+  const char* hdrs[] = {kOtpwHeader};
+  const char* hdr_names[] = {"pmg_otpw.cuh"};
+  if (nvrtcCreateProgram(&prog, source.c_str(), src_path.c_str(), 1, hdrs, hdr_names) != NVRTC_SUCCESS)
+    throw Error(-7, "nvrtcCreateProgram failed");
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof kOptions / sizeof kOptions[0]), kOptions);
+  size_t ls = 0;
+  nvrtcGetProgramLogSize(prog, &ls);
+  c.log.resize(ls);
+  if (ls) nvrtcGetProgramLog(prog, &c.log[0]);
+  if (r != NVRTC_SUCCESS) {
+    std::string m = "NVRTC compilation of " + name + " failed: " + c.log.substr(0, 4000);
+    nvrtcDestroyProgram(&prog);
+    throw Error(-7, m);
+  }
+  size_t cs = 0;
+  nvrtcGetCUBINSize(prog, &cs);
+  c.cubin.resize(cs);
+  nvrtcGetCUBIN(prog, c.cubin.data());
+  nvrtcDestroyProgram(&prog);
+  c.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  parse_ptxas(c);
+  {
+    std::ofstream f(base + ".cubin.tmp", std::ios::binary);
+    f.write(c.cubin.data(), (std::streamsize)c.cubin.size());
+  }
+  { std::ofstream f(base + ".log"); f << c.log; }
+  std::rename((base + ".cubin.tmp").c_str(), (base + ".cubin").c_str());
+  return c;
+}
+
+// -------------------------------------------------------------------------------------------- plans
+static void check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw Error(-6, std::string(what) + ": " + cu_err(r));
+}
+
+struct CtxGuard {   // make the plan's primary context current for the duration of a call
+  CUcontext prev = nullptr;
+  bool active = false;
+  explicit CtxGuard(CUcontext c) {
+    drv().CtxGetCurrent(&prev);
+    if (prev != c) { drv().CtxSetCurrent(c); active = true; }
+  }
+  ~CtxGuard() { if (active) drv().CtxSetCurrent(prev); }
+};
+
+static int64_t round_up64(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
+
+std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,
+                                  const pmg_gpu_spec* spec, const pmg_weights* w, const pmg_sched_opts* opts) {
+  Drv& D = drv();
+  if (!D.ok) throw Error(-6, D.err);
+  auto P = std::make_unique<Plan>();
+  P->pipe = p;
+  P->A = analyze(*p, params);
+  P->device = device;
+  CUdevice dev;
+  check(D.DeviceGet(&dev, device), "cuDeviceGet");
+  check(D.DevicePrimaryCtxRetain(&P->ctx, dev), "cuDevicePrimaryCtxRetain");
+  CtxGuard guard(P->ctx);
+  if (spec) P->spec = *spec;
+  else {
+    gpu_preset("b200", &P->spec);
+    int v;
+    if (D.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev) == CUDA_SUCCESS) P->spec.nsms = v;
+    if (D.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_MULTIPROCESSOR, dev) == CUDA_SUCCESS) P->spec.shmem_per_sm = v;
+    if (D.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_BLOCK_OPTIN, dev) == CUDA_SUCCESS) P->spec.max_shmem_per_tb = v;
+    if (D.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE, dev) == CUDA_SUCCESS) P->spec.l2_bytes = v;
+  }
+  if (w) P->weights = *w;
+  else weights_preset("b200", &P->weights);
+  pmg_sched_opts o;
+  if (opts) o = *opts;
+  else {
+    std::memset(&o, 0, sizeof o);
+    o.vec = o.chunks = o.rows = o.warps = o.prefetch = o.tx_size = -1;
+    o.smem_chunks = -1;
+    o.fuse = 1;
+  }
+  P->sch = schedule(P->A, P->spec, P->weights, o);
+  const Pipeline& pp = *p;
+  P->nimages = (int)pp.images.size();
+  P->ntables = (int)pp.tables.size();
+  P->nout = (int)pp.liveouts.size();
+  // workspace: every materialised stage that is not a liveout
+  size_t off = 0;
+  for (auto& g : P->sch.groups)
+    for (auto& s : g.gs) {
+      if (!s.materialize) continue;
+      if (std::find(pp.liveouts.begin(), pp.liveouts.end(), s.id) != pp.liveouts.end()) continue;
+      const Ext3& e = P->A.stage_ext[s.id];
+      WsTensor t;
+      t.stage = s.id;
+      t.row_pitch = round_up64(e.e[2] * dtype_size(pp.stages[s.id].dtype), 128);
+      t.rows = e.e[1];
+      t.planes = e.e[0];
+      t.plane_pitch = t.row_pitch * t.rows;
+      t.offset = off;
+      off += (size_t)round_up64(t.plane_pitch * t.planes, 256);
+      P->ws.push_back(t);
+    }
+  P->ws_bytes = off;
+  // compile + load
+  std::ostringstream js;
+  js << "{\"schedule\":" << P->sch.json << ",\"kernels\":[";
+  for (size_t gi = 0; gi < P->sch.groups.size(); ++gi) {
+    Group& g = P->sch.groups[gi];
+    g.source = emit_group(P->A, g);
+    Kernel k;
+    k.bin = jit_compile(g.name, g.source);
+    check(D.ModuleLoadData(&k.mod, k.bin.cubin.data()), "cuModuleLoadData");
+    check(D.ModuleGetFunction(&k.fn, k.mod, g.name.c_str()), "cuModuleGetFunction");
+    if (g.block_smem > 48 * 1024)
+      check(D.FuncSetAttribute(k.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, g.block_smem), "cuFuncSetAttribute");
+    check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm, k.fn, g.cfg.NW * 32, g.block_smem), "occupancy");
+    if (k.blocks_per_sm < 1) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
+    js << (gi ? "," : "") << "{\"name\":\"" << g.name << "\",\"regs\":" << k.bin.regs << ",\"spill_stores\":"
+       << k.bin.spill_stores << ",\"spill_loads\":" << k.bin.spill_loads << ",\"block_smem\":" << g.block_smem
+       << ",\"blocks_per_sm\":" << k.blocks_per_sm << ",\"cached\":" << (k.bin.from_cache ? "true" : "false")
+       << ",\"compile_s\":" << k.bin.compile_s << "}";
+    P->kernels.push_back(std::move(k));
+  }
+  js << "],\"workspace_bytes\":" << P->ws_bytes << "}";
+  P->json = js.str();
+  return P;
+}
+
+void plan_destroy(Plan* P) {
+  if (!P) return;
+  if (drv().ok && P->ctx) {
+    CtxGuard g(P->ctx);
+    for (auto& k : P->kernels)
+      if (k.mod) drv().ModuleUnload(k.mod);
+    CUdevice dev;
+    if (drv().DeviceGet(&dev, P->device) == CUDA_SUCCESS) drv().DevicePrimaryCtxRelease(dev);
+  }
+}
+
+// ---------------------------------------------------------------------------------- band geometry
+// rows needed of every stage / image for liveout rows [r0, r1) (cumulative halo, clipped)
+struct Need { std::vector<RowIv> stage, image; };
+
+static Need rows_for(const Plan& P, int64_t r0, int64_t r1) {
+  const Pipeline& p = *P.pipe;
+  const Analysis& A = P.A;
+  Need n;
+  n.stage.assign(p.stages.size(), RowIv{0, 0});
+  n.image.assign(p.images.size(), RowIv{0, 0});
+  auto hull = [](RowIv& a, RowIv b) {
+    if (b.hi <= b.lo) return;
+    if (a.hi <= a.lo) a = b;
+    else { a.lo = std::min(a.lo, b.lo); a.hi = std::max(a.hi, b.hi); }
+  };
+  for (int lo : p.liveouts) hull(n.stage[lo], RowIv{r0, r1});
+  for (int ti = (int)p.topo.size() - 1; ti >= 0; --ti) {
+    int c = p.topo[ti];
+    if (n.stage[c].hi <= n.stage[c].lo) continue;
+    for (int ri : A.reads_of[c]) {
+      const ReadSite& r = A.reads[ri];
+      int64_t rows = r.src_is_stage ? A.stage_ext[r.src].e[1] : A.image_ext[r.src].e[1];
+      RowIv need = rows_needed(A, r, n.stage[c], rows);
+      if (r.src_is_stage) hull(n.stage[r.src], need);
+      else hull(n.image[r.src], need);
+    }
+  }
+  // group granularity: every stage of a group computes the group's row range
+  for (auto& g : P.sch.groups) {
+    RowIv h{0, 0};
+    for (auto& s : g.gs) hull(h, n.stage[s.id]);
+    for (auto& s : g.gs) n.stage[s.id] = h;
+  }
+  return n;
+}
+
+BandRows band_rows(const Plan& P, int band, int nbands) {
+  const Pipeline& p = *P.pipe;
+  int64_t H = P.A.stage_ext[p.liveouts[0]].e[1];
+  for (int lo : p.liveouts)
+    if (P.A.stage_ext[lo].e[1] != H) throw Error(-3, "band mode needs liveouts of equal row extent");
+  BandRows b;
+  b.out_r0 = band * H / nbands;
+  b.out_r1 = (band + 1) * H / nbands;
+  Need n = rows_for(P, b.out_r0, b.out_r1);
+  b.in_r0 = INT64_MAX;
+  b.in_r1 = INT64_MIN;
+  for (size_t i = 0; i < p.images.size(); ++i) {
+    if (n.image[i].hi <= n.image[i].lo) continue;
+    b.in_r0 = std::min(b.in_r0, n.image[i].lo);
+    b.in_r1 = std::max(b.in_r1, n.image[i].hi);
+  }
+  if (b.in_r0 == INT64_MAX) { b.in_r0 = 0; b.in_r1 = 0; }
+  return b;
+}
+
+// ------------------------------------------------------------------------------------------ launch
+#pragma pack(push, 1)
+struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, pad; };
+#pragma pack(pop)
+static_assert(sizeof(HostTensor) == 40, "PmgTensor mirror");
+
+void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* ws, CUstream s, int band,
+              int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs) {
+  Drv& D = drv();
+  if (!D.ok) throw Error(-6, D.err);
+  const Pipeline& p = *P.pipe;
+  const Analysis& A = P.A;
+  if (nin != P.nimages + P.ntables) throw Error(-9, "expected " + std::to_string(P.nimages + P.ntables) + " inputs");
+  if (nout != P.nout) throw Error(-9, "expected " + std::to_string(P.nout) + " outputs");
+  CUcontext cur = nullptr;
+  D.CtxGetCurrent(&cur);
+  CUdevice cd;
+  if (!cur || D.CtxGetDevice(&cd) != CUDA_SUCCESS || (int)cd != P.device)
+    throw Error(-9, "the plan's device must be current on the calling thread");
+  if (P.ws_bytes && !ws) throw Error(-9, "workspace required");
+  auto aligned = [](const pmg_buf& b) {
+    return ((uintptr_t)b.ptr % 16 == 0) && (b.row_pitch_bytes % 16 == 0) && (b.plane_pitch_bytes % 16 == 0);
+  };
+  for (int i = 0; i < P.nimages; ++i)
+    if (!in[i].ptr || !aligned(in[i])) throw Error(-9, "input " + p.images[i].name + " is NULL or not 16-byte aligned");
+  for (int i = 0; i < nout; ++i)
+    if (!out[i].ptr || !aligned(out[i])) throw Error(-9, "output " + p.stages[p.liveouts[i]].name + " is NULL or not 16-byte aligned");
+  if ((uintptr_t)ws % 16) throw Error(-9, "workspace not 16-byte aligned");
+  int64_t r0 = 0, r1 = 0;
+  Need need;
+  bool banded = band >= 0;
+  if (banded) {
+    BandRows br = band_rows(P, band, nbands);
+    r0 = br.out_r0;
+    r1 = br.out_r1;
+    if (r1 <= r0) return;
+    need = rows_for(P, r0, r1);
+    for (auto& g : P.sch.groups)
+      for (auto& st : g.gs)
+        if (std::find(p.liveouts.begin(), p.liveouts.end(), st.id) != p.liveouts.end() && !p.consumers[st.id].empty())
+          throw Error(-3, "band mode: a liveout that is also consumed by the pipeline is not supported");
+  }
+  int64_t in_row_base = banded ? band_rows(P, band, nbands).in_r0 : 0;
+  for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) {
+    const Group& g = P.sch.groups[gi];
+    Kernel& K = P.kernels[gi];
+    const int NT = std::max<int>(1, (int)g.tensors.size()), NTAB = std::max(1, P.ntables),
+              NP = std::max<int>(1, (int)p.params.size());
+    size_t off_tab = 40 * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
+           off_int = off_prm + 4 * NP, size = (off_int + 40 + 7) / 8 * 8;
+    std::vector<char> buf(size, 0);
+    for (size_t ti = 0; ti < g.tensors.size(); ++ti) {
+      auto [is_stage, id] = g.tensors[ti];
+      HostTensor t{};
+      if (!is_stage) {
+        t.ptr = (uint64_t)(uintptr_t)in[id].ptr;
+        t.rp = in[id].row_pitch_bytes;
+        t.pp = in[id].plane_pitch_bytes;
+        t.fs = in_fs ? in_fs[id] : 0;
+        t.row_base = (int32_t)(banded ? in_row_base : 0);
+      } else {
+        auto lit = std::find(p.liveouts.begin(), p.liveouts.end(), id);
+        if (lit != p.liveouts.end()) {
+          int oi = int(lit - p.liveouts.begin());
+          t.ptr = (uint64_t)(uintptr_t)out[oi].ptr;
+          t.rp = out[oi].row_pitch_bytes;
+          t.pp = out[oi].plane_pitch_bytes;
+          t.fs = out_fs ? out_fs[oi] : 0;
+          t.row_base = (int32_t)(banded ? r0 : 0);
+        } else {
+          const WsTensor* w = nullptr;
+          for (auto& x : P.ws)
+            if (x.stage == id) w = &x;
+          if (!w) throw Error(-2, "internal: no workspace for " + p.stages[id].name);
+          t.ptr = (uint64_t)(uintptr_t)((char*)ws + w->offset);
+          t.rp = w->row_pitch;
+          t.pp = w->plane_pitch;
+          t.fs = (int64_t)P.ws_bytes;
+          t.row_base = (int32_t)(banded ? need.stage[id].lo : 0);
+        }
+      }
+      std::memcpy(buf.data() + 40 * ti, &t, 40);
+    }
+    for (int ti = 0; ti < P.ntables; ++ti) {
+      uint64_t ptr = (uint64_t)(uintptr_t)in[P.nimages + ti].ptr;
+      int32_t n = (int32_t)A.table_len[ti];
+      std::memcpy(buf.data() + off_tab + 8 * ti, &ptr, 8);
+      std::memcpy(buf.data() + off_tabn + 4 * ti, &n, 4);
+    }
+    for (size_t pi = 0; pi < p.params.size(); ++pi) {
+      int32_t v = (int32_t)A.params[pi];
+      std::memcpy(buf.data() + off_prm + 4 * pi, &v, 4);
+    }
+    int32_t Hg = (int32_t)g.ext.e[1], Wg = (int32_t)g.ext.e[2];
+    int32_t gy0 = 0, gy1 = Hg;
+    if (banded) {
+      RowIv h = need.stage[g.gs[0].id];
+      gy0 = (int32_t)h.lo;
+      gy1 = (int32_t)h.hi;
+    }
+    if (gy1 <= gy0) continue;
+    int64_t nty = (gy1 - gy0 + g.cfg.TH - 1) / g.cfg.TH;
+    int64_t ntiles = (int64_t)nframes * g.npl * nty * g.ntx;
+    if (ntiles > INT32_MAX) throw Error(-3, "too many tiles");
+    int32_t ints[10] = {Hg, Wg, gy0, gy1, (int32_t)nty, (int32_t)g.ntx, (int32_t)g.npl, (int32_t)nframes, (int32_t)ntiles, 0};
+    std::memcpy(buf.data() + off_int, ints, 40);
+    int64_t blocks_needed = (ntiles + g.cfg.NW - 1) / g.cfg.NW;
+    int64_t grid = std::min<int64_t>(blocks_needed, (int64_t)K.blocks_per_sm * P.spec.nsms);
+    void* args[] = {buf.data()};
+    CUresult r = D.LaunchKernel(K.fn, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, s, args, nullptr);
+    if (r != CUDA_SUCCESS) throw Error(-6, "launch of " + g.name + ": " + cu_err(r));
+  }
+}
+
+}  // namespace pmg

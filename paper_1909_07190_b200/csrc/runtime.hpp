@@ -1,0 +1,65 @@
+// runtime.hpp — JIT compilation (NVRTC, sm_100a), plans, workspace and stream-ordered launches.
+#pragma once
+#include <cuda.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "select.hpp"
+
+namespace pmg {
+
+struct Compiled {
+  std::string name, source, log;
+  std::vector<char> cubin;
+  int regs = -1, spill_stores = -1, spill_loads = -1, smem_static = -1;
+  bool from_cache = false;
+  double compile_s = 0;
+};
+
+// compile one group kernel for sm_100a (disk cache keyed by source + options); throws Error(PMG_ERR_NVRTC)
+Compiled jit_compile(const std::string& name, const std::string& source);
+
+struct WsTensor {          // workspace placement of an intermediate (materialised, non-liveout) stage
+  int stage = -1;
+  size_t offset = 0;
+  int64_t row_pitch = 0, plane_pitch = 0, rows = 0, planes = 0;
+};
+
+struct Kernel {
+  Compiled bin;
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  int blocks_per_sm = 0;
+};
+
+struct Plan {
+  std::shared_ptr<Pipeline> pipe;
+  Analysis A;
+  Schedule sch;
+  pmg_gpu_spec spec;
+  pmg_weights weights;
+  int device = -1;
+  CUcontext ctx = nullptr;
+  std::vector<Kernel> kernels;
+  std::vector<WsTensor> ws;
+  size_t ws_bytes = 0;
+  int nimages = 0, ntables = 0, nout = 0;
+  std::string json;
+};
+
+std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,
+                                  const pmg_gpu_spec* spec, const pmg_weights* w, const pmg_sched_opts* opts);
+void plan_destroy(Plan* plan);
+
+struct BandRows { int64_t out_r0, out_r1, in_r0, in_r1; };
+BandRows band_rows(const Plan& P, int band, int nbands);
+
+// launch every group kernel; band < 0: full image; nframes >= 1 (batch)
+void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace, CUstream s,
+              int band, int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs);
+
+std::string kernel_dir();   // directory of libpmg.so (for the cubin cache)
+
+}  // namespace pmg

@@ -1,0 +1,478 @@
+// select.cpp — the GPU cost model of Alg. 2, its argmin (line 1015) and DP fusion
+// (§2.4; Bounded DP-Fusion lines 1347-1349).
+//
+// Two instantiations of the same cost function:
+//   paper mode (paper_analyze_group): the paper's own geometry — warp sizes, warp overlapped
+//     tile, scratchpads prod ceil(B_i/W_i)(T_i W_i + O_i^n), used to pin the §3/§4
+//     worked examples on the GTX 1080Ti / V100 presets of Table 1;
+//   B200 mode (b200_cost): the same seven terms evaluated on this library's kernel (KConfig): shared memory
+//     = the TMA ring, registers = the register windows, transactions = TMA row copies.
+// Readings of the garbled / undefined symbols (R13-R16):
+//   R13 regTile = round(T_split * fracReg) registers per buffered stage per thread (Alg. 1 l.867);
+//   R14 tileVol at l.953 = iterations of the load's loop per warp tile; totalTB = tbPerSM (l.939);
+//       warpBW = GlMemBW * WarpSize / (NSMs * CoresPerSM) (text P:1081-1083); the w1 term is normalised per
+//       output point so that it is O(1) like the other terms;
+//   R15 MaxThPerSM = 2048; R16 fracReg grid = integer register-chunk counts (dedupe of {0,0.1,..,1}*T).
+#include "select.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <sstream>
+
+namespace pmg {
+
+static void set_name(pmg_gpu_spec* s, const char* n) {
+  std::memset(s->name, 0, sizeof s->name);
+  std::strncpy(s->name, n, sizeof s->name - 1);
+}
+
+bool gpu_preset(const std::string& name, pmg_gpu_spec* s) {
+  std::memset(s, 0, sizeof *s);
+  s->warp_size = 32;
+  s->max_threads_per_sm = 2048;        // R15 (absent from Table 1)
+  s->gl_tx_size[0] = 32;
+  s->gl_tx_size[1] = 128;
+  s->max_warps_per_sm = 64;
+  s->regs_per_sm = 65536;
+  if (name == "gtx1080ti") {           // Table 1
+    set_name(s, "gtx1080ti");
+    s->nsms = 28; s->cores_per_sm = 128; s->gl_mem_bw = 484e9;
+    s->max_shmem_per_tb = 48 * 1024; s->shmem_per_sm = 96 * 1024;
+    s->max_tb_per_sm = 16; s->max_regs_per_thread = 256;
+    s->l2_bytes = 2816 * 1024; s->sm_clock_hz = 1.58e9;
+    return true;
+  }
+  if (name == "teslav100") {
+    set_name(s, "teslav100");
+    s->nsms = 80; s->cores_per_sm = 64; s->gl_mem_bw = 898e9;
+    s->max_shmem_per_tb = 96 * 1024; s->shmem_per_sm = 96 * 1024;
+    s->max_tb_per_sm = 32; s->max_regs_per_thread = 256;
+    s->l2_bytes = 6 * 1024 * 1024; s->sm_clock_hz = 1.53e9;
+    return true;
+  }
+  if (name == "b200") {                // SURVEY §7.3; GlMemBW = measured copy bandwidth (MEASURED_PEAKS.json)
+    set_name(s, "b200");
+    s->nsms = 148; s->cores_per_sm = 128; s->gl_mem_bw = 6538.6e9;
+    s->max_shmem_per_tb = 227 * 1024; s->shmem_per_sm = 228 * 1024;
+    s->max_tb_per_sm = 32; s->max_regs_per_thread = 255;
+    s->l2_bytes = 126LL * 1024 * 1024; s->sm_clock_hz = 1.965e9;
+    return true;
+  }
+  return false;
+}
+
+bool weights_preset(const std::string& name, pmg_weights* w) {
+  // Table 3; the B200 row starts from the V100 row (weight refit is NEXT-3)
+  static const double t1080[7] = {50, 0.5, 45, 20, 2, 100, 1};
+  static const double v100[7] = {50, 0.5, 60, 10, 2, 100, 1};
+  const double* src = name == "gtx1080ti" ? t1080 : (name == "teslav100" || name == "b200") ? v100 : nullptr;
+  if (!src) return false;
+  for (int i = 0; i < 7; ++i) w->w[i] = src[i];
+  return true;
+}
+
+// ---- static profile: operation count of a stage body per point (TimePerIter proxy) ----
+static double ops_of(const Expr& e) {
+  double c = 0;
+  for (auto& a : e.args) c += ops_of(*a);
+  switch (e.op) {
+    case Expr::BIN:
+      if (e.text == "/") return c + (e.kind == Kind::Float ? 8 : 20);
+      if (e.text == "%") return c + 20;
+      return c + 1;
+    case Expr::UN: return c + 1;
+    case Expr::CALL:
+      if (e.text == "sqrt") return c + 8;
+      if (e.text == "lerp") return c + 3;
+      if (e.text == "clamp") return c + 2;
+      return c + 1;
+    case Expr::TABLE: return c + 4;
+    default: return c;
+  }
+}
+
+double stage_ops(const Pipeline& p, int s) { return std::max(1.0, ops_of(*p.stages[s].expr)); }
+
+// ---- the shared tail of Alg. 2 (lines 957-982) ----
+static void alg2_tail(CostBreakdown& c, const pmg_gpu_spec& S, const pmg_weights& w, double tile_vol,
+                      double time_per_iter_sum, double overlap_pts, double computed_pts, int tx_size) {
+  if (c.sh_mem_per_tb > S.max_shmem_per_tb) { c.infinite = true; c.why = "shMemPerTB > MaxShMemPerTb"; }
+  c.max_tb_per_sm = std::min(c.sh_mem_per_tb > 0 ? std::floor(S.shmem_per_sm / c.sh_mem_per_tb) : (double)S.max_tb_per_sm,
+                             (double)S.max_tb_per_sm);                                                         // l.957
+  c.sh_mem_occ = std::min(c.max_tb_per_sm * c.warps_per_tb, (double)S.max_warps_per_sm);                      // l.958
+  if (c.reg_per_th > S.max_regs_per_thread) { c.infinite = true; c.why = "regPerTh > MaxRegPerTh"; }           // l.961
+  double max_th = std::min(std::floor(S.regs_per_sm / std::max(1.0, c.reg_per_th)), (double)S.max_threads_per_sm);  // l.963
+  c.reg_occ = std::floor(max_th / S.warp_size);                                                               // l.965
+  c.occupancy = std::min(c.sh_mem_occ, c.reg_occ) / S.max_warps_per_sm;                                      // l.966
+  c.warp_bw = S.gl_mem_bw * S.warp_size / (S.nsms * (double)S.cores_per_sm);                                 // l.967 (R14)
+  c.mem_time = tx_size * c.total_gl_txs / c.warp_bw;                                                          // l.970
+  c.compute_time = time_per_iter_sum * tile_vol;                                                              // l.972
+  double shm_per_sm = c.sh_mem_per_tb * c.max_tb_per_sm;                                                      // l.975
+  c.unallocated_sh_mem = std::max(0.0, std::min(1.0, 1.0 - shm_per_sm / S.shmem_per_sm));                    // l.976
+  double reg_per_sm = c.reg_per_th * S.max_warps_per_sm * S.warp_size;                                        // l.977
+  c.unused_reg = std::max(0.0, std::min(1.0, 1.0 - reg_per_sm * c.occupancy / S.regs_per_sm));               // l.978
+  c.frac_overlap = computed_pts > 0 ? overlap_pts / computed_pts : 0.0;                                       // l.979 (R12)
+  c.extra_tbs = c.max_tb_per_sm > 0 ? std::fmod(std::ceil(c.tb_per_sm), c.max_tb_per_sm) : 0;                // l.980 (R14)
+  double ratio = c.compute_time > 0 ? c.mem_time / c.compute_time : 0;
+  c.cost = w.w[0] * c.txs_per_point + w.w[1] * (1 - c.occupancy) + w.w[2] * ratio + w.w[3] * c.unallocated_sh_mem +
+           w.w[4] * c.unused_reg + w.w[5] * c.frac_overlap + w.w[6] * c.extra_tbs;                            // l.981
+  if (c.infinite) c.cost = std::numeric_limits<double>::infinity();
+}
+
+// transactions of one warp access of `n` consecutive elements of `esz` bytes starting at byte `start` (MinGLTxs)
+static double min_txs(int64_t start, int64_t nbytes, int tx) {
+  if (nbytes <= 0) return 0;
+  int64_t a = (int64_t)std::floor((double)start / tx), b = (int64_t)std::floor((double)(start + nbytes - 1) / tx);
+  return double(b - a + 1);
+}
+
+CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S, const pmg_weights& w) {
+  const Pipeline& p = *A.p;
+  const KConfig& k = g.cfg;
+  CostBreakdown c;
+  const double H = (double)g.ext.e[1], W = (double)g.ext.e[2], C = (double)g.npl;
+  const double tiles = C * std::ceil(H / k.TH) * std::ceil(W / g.OW);
+  c.total_threads = tiles * 32;
+  c.warps_per_tb = k.NW;
+  c.tb_per_sm = tiles / k.NW / S.nsms;                                                                         // l.939
+  c.sh_mem_per_tb = g.block_smem;                                                                              // l.942-943
+  c.reg_tile = 0;
+  c.reg_per_th = g.regs_est;                                                                                   // l.960
+  // global transactions per warp tile: TMA row copies of every stream + gathers + output rows
+  double txs = 0;
+  for (auto& st : g.streams) {
+    double rows = k.TH + st.hi - st.lo;
+    txs += rows * min_txs(0, (int64_t)st.row_elems * st.esz, k.tx_size);
+  }
+  double out_pts = (double)g.OW * k.TH;
+  for (size_t r = 0; r < g.greads.size(); ++r)
+    if (g.greads[r].kind == RKind::GATHER) txs += out_pts / 8.0;     // ~one 32B sector per 8 scattered elements
+  c.total_gl_txs = txs;
+  c.txs_per_point = txs * k.tx_size / 32.0 / out_pts;   // in 32-byte sector units per output point
+  double tpi = 0, computed = 0, useful = 0;
+  for (auto& P : g.gs) {
+    double pts = (double)g.CW * (k.TH + P.hi - P.lo);
+    double t = stage_ops(p, P.id) / S.sm_clock_hz;
+    tpi += t * pts / (double)(g.CW * k.TH);
+    computed += pts;
+    useful += out_pts;
+  }
+  alg2_tail(c, S, w, (double)g.CW * k.TH, tpi, computed - useful, computed, k.tx_size);
+  return c;
+}
+
+static bool feasible_stage_set(const Analysis& A, const std::vector<int>& stages) {
+  // cheap pre-check: same extents
+  for (int s : stages)
+    if (!(A.stage_ext[s] == A.stage_ext[stages[0]])) return false;
+  return true;
+}
+
+bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const pmg_gpu_spec& S, const pmg_weights& w,
+                 const pmg_sched_opts& o, CostBreakdown* out) {
+  std::vector<int> Vs = o.vec > 0 ? std::vector<int>{o.vec} : std::vector<int>{1, 2, 4};
+  std::vector<int> TXs = o.chunks > 0 ? std::vector<int>{o.chunks} : std::vector<int>{1, 2, 4};
+  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 32, 64};
+  std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{2, 4, 8};
+  std::vector<int> PFs = o.prefetch > 0 ? std::vector<int>{o.prefetch} : std::vector<int>{2, 4};
+  std::vector<int> TXSZ = o.tx_size > 0 ? std::vector<int>{o.tx_size} : std::vector<int>{32, 128};
+  std::vector<int> Ss = o.smem_chunks >= 0 ? std::vector<int>{o.smem_chunks} : std::vector<int>{0};
+  bool found = false;
+  Group best;
+  CostBreakdown bc;
+  std::string why = "no candidate";
+  long count = 0;
+  for (int V : Vs)
+    for (int TX : TXs)
+      for (int S_ : Ss)
+        for (int TH : THs)
+          for (int NW : NWs)
+            for (int PF : PFs)
+              for (int tx : TXSZ) {
+                if (o.budget > 0 && count >= o.budget) break;
+                Group cand;
+                cand.stages = g.stages;
+                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx};
+                if (S_ > TX) continue;
+                ++count;
+                if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
+                CostBreakdown c = b200_cost(A, cand, S, w);
+                if (c.infinite) { why = c.why; continue; }
+                auto vol = [](const KConfig& q) { return (double)q.V * q.TX * q.TH; };
+                bool better = !found || c.cost < bc.cost - 1e-12 ||
+                              (std::fabs(c.cost - bc.cost) <= 1e-12 &&     // tie-break
+                               (vol(cand.cfg) < vol(best.cfg) ||
+                                (vol(cand.cfg) == vol(best.cfg) &&
+                                 (cand.cfg.NW < best.cfg.NW ||
+                                  (cand.cfg.NW == best.cfg.NW && (cand.cfg.S > best.cfg.S ||
+                                                                  (cand.cfg.S == best.cfg.S && cand.cfg.tx_size > best.cfg.tx_size)))))));
+                if (better) { best = cand; bc = c; found = true; }
+              }
+  if (!found) { g.why_infeasible = why; return false; }
+  g = best;
+  if (out) *out = bc;
+  return true;
+}
+
+Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w, const pmg_sched_opts& o) {
+  const Pipeline& p = *A.p;
+  const int n = (int)p.stages.size();
+  Schedule sch;
+  auto name_groups = [&](Schedule& s) {
+    for (size_t i = 0; i < s.groups.size(); ++i) s.groups[i].name = "pmg_g" + std::to_string(i);
+  };
+  if (o.group_of_stage) {
+    // explicit grouping: one group per distinct index, ordered by first topological occurrence
+    std::vector<int> gos(o.group_of_stage, o.group_of_stage + n);
+    std::vector<int> seen;
+    for (int s : p.topo)
+      if (std::find(seen.begin(), seen.end(), gos[s]) == seen.end()) seen.push_back(gos[s]);
+    sch.group_of_stage = gos;
+    std::ostringstream js;
+    js << "{\"mode\":\"manual\",\"groups\":[";
+    for (size_t gi = 0; gi < seen.size(); ++gi) {
+      Group g;
+      for (int s : p.topo)
+        if (gos[s] == seen[gi]) g.stages.push_back(s);
+      CostBreakdown cb;
+      if (!best_config(A, g, gos, S, w, o, &cb))
+        throw Error(PMG_ERR_INFEASIBLE, "group " + std::to_string(gi) + ": " + g.why_infeasible);
+      g.name = "pmg_g" + std::to_string(gi);
+      js << (gi ? "," : "") << "{\"config\":" << config_json(A, g) << ",\"cost\":" << cost_json(cb) << "}";
+      sch.groups.push_back(g);
+    }
+    js << "]}";
+    sch.json = js.str();
+    name_groups(sch);
+    return sch;
+  }
+  // DP over contiguous runs of the topological order (each run is convex): best[j] = min_i best[i] + cost(i..j)
+  const double INF = std::numeric_limits<double>::infinity();
+  std::vector<double> best(n + 1, INF);
+  std::vector<int> from(n + 1, -1);
+  std::vector<std::vector<Group>> seg_group(n + 1, std::vector<Group>(n + 1));
+  std::vector<std::vector<double>> seg_cost(n + 1, std::vector<double>(n + 1, INF));
+  std::vector<std::vector<CostBreakdown>> seg_cb(n + 1, std::vector<CostBreakdown>(n + 1));
+  best[0] = 0;
+  const bool fuse = o.fuse != 0;
+  for (int j = 1; j <= n; ++j) {
+    for (int i = j - 1; i >= 0; --i) {
+      if (!fuse && j - i > 1) break;
+      if (best[i] == INF) continue;
+      std::vector<int> seg(p.topo.begin() + i, p.topo.begin() + j);
+      if (!feasible_stage_set(A, seg)) continue;
+      // grouping vector: stages of seg in group 0, every other stage in its own group
+      std::vector<int> gos(n);
+      for (int s = 0; s < n; ++s) gos[s] = s + 1;
+      for (int s : seg) gos[s] = 0;
+      Group g;
+      g.stages = seg;
+      CostBreakdown cb;
+      if (!best_config(A, g, gos, S, w, o, &cb)) continue;
+      seg_group[i][j] = g;
+      seg_cost[i][j] = cb.cost;
+      seg_cb[i][j] = cb;
+      if (best[i] + cb.cost < best[j]) { best[j] = best[i] + cb.cost; from[j] = i; }
+    }
+    if (best[j] == INF) throw Error(PMG_ERR_INFEASIBLE, "no feasible group ends at stage " + p.stages[p.topo[j - 1]].name);
+  }
+  std::vector<std::pair<int, int>> segs;
+  for (int j = n; j > 0; j = from[j]) segs.push_back({from[j], j});
+  std::reverse(segs.begin(), segs.end());
+  sch.group_of_stage.assign(n, -1);
+  for (size_t gi = 0; gi < segs.size(); ++gi)
+    for (int q = segs[gi].first; q < segs[gi].second; ++q) sch.group_of_stage[p.topo[q]] = (int)gi;
+  std::ostringstream js;
+  js << "{\"mode\":\"dp\",\"total_cost\":" << best[n] << ",\"groups\":[";
+  for (size_t gi = 0; gi < segs.size(); ++gi) {
+    Group g = seg_group[segs[gi].first][segs[gi].second];
+    // rebuild with the final grouping (materialisation depends on the other groups)
+    Group h;
+    h.stages = g.stages;
+    h.cfg = g.cfg;
+    if (!build_group(A, h, sch.group_of_stage)) throw Error(PMG_ERR_INFEASIBLE, h.why_infeasible);
+    h.name = "pmg_g" + std::to_string(gi);
+    CostBreakdown cb = b200_cost(A, h, S, w);
+    js << (gi ? "," : "") << "{\"config\":" << config_json(A, h) << ",\"cost\":" << cost_json(cb) << "}";
+    sch.groups.push_back(h);
+  }
+  js << "]}";
+  sch.json = js.str();
+  return sch;
+}
+
+std::string cost_json(const CostBreakdown& c) {
+  std::ostringstream o;
+  o.precision(10);
+  auto num = [&](double v) { if (std::isinf(v)) o << "\"inf\""; else o << v; };
+  o << "{\"totalThreads\":"; num(c.total_threads);
+  o << ",\"warpsPerTB\":"; num(c.warps_per_tb);
+  o << ",\"tbPerSM\":"; num(c.tb_per_sm);
+  o << ",\"shMemPerTB\":"; num(c.sh_mem_per_tb);
+  o << ",\"regTile\":"; num(c.reg_tile);
+  o << ",\"regPerTh\":"; num(c.reg_per_th);
+  o << ",\"totalGLMemTxs\":"; num(c.total_gl_txs);
+  o << ",\"txsPerPoint\":"; num(c.txs_per_point);
+  o << ",\"maxTBPerSM\":"; num(c.max_tb_per_sm);
+  o << ",\"shMemOcc\":"; num(c.sh_mem_occ);
+  o << ",\"regOcc\":"; num(c.reg_occ);
+  o << ",\"occupancy\":"; num(c.occupancy);
+  o << ",\"warpBW\":"; num(c.warp_bw);
+  o << ",\"memTime\":"; num(c.mem_time);
+  o << ",\"computeTime\":"; num(c.compute_time);
+  o << ",\"unallocatedShMem\":"; num(c.unallocated_sh_mem);
+  o << ",\"unusedReg\":"; num(c.unused_reg);
+  o << ",\"fracOverlap\":"; num(c.frac_overlap);
+  o << ",\"extraTBs\":"; num(c.extra_tbs);
+  o << ",\"cost\":"; num(c.cost);
+  o << ",\"infinite\":" << (c.infinite ? "true" : "false") << ",\"why\":\"" << c.why << "\"}";
+  return o.str();
+}
+
+std::string config_json(const Analysis& A, const Group& g) {
+  const Pipeline& p = *A.p;
+  const KConfig& k = g.cfg;
+  std::ostringstream o;
+  o << "{\"name\":\"" << g.name << "\",\"stages\":[";
+  for (size_t i = 0; i < g.gs.size(); ++i) o << (i ? "," : "") << "\"" << p.stages[g.gs[i].id].name << "\"";
+  o << "],\"V\":" << k.V << ",\"TX\":" << k.TX << ",\"S\":" << k.S << ",\"TH\":" << k.TH << ",\"NW\":" << k.NW
+    << ",\"PREF\":" << k.PREF << ",\"txSz\":" << k.tx_size << ",\"fracReg\":" << double(k.TX - k.S) / k.TX
+    << ",\"tile\":[" << k.V * k.TX << "," << k.TH << ",1],\"block\":[" << 32 * k.NW << ",1,1],\"warp\":[32,1,1]"
+    << ",\"CW\":" << g.CW << ",\"OW\":" << g.OW << ",\"PL\":" << g.PL << ",\"PR\":" << g.PR << ",\"t_first\":" << g.t_first
+    << ",\"unroll\":" << g.U << ",\"warp_smem\":" << g.warp_smem << ",\"regs_est\":" << g.regs_est << ",\"stage_geom\":[";
+  for (size_t i = 0; i < g.gs.size(); ++i) {
+    auto& P = g.gs[i];
+    o << (i ? "," : "") << "{\"stage\":\"" << p.stages[P.id].name << "\",\"hi\":" << P.hi << ",\"lo\":" << P.lo
+      << ",\"window\":" << P.depth << ",\"ext\":[" << P.el << "," << P.er << "],\"invalid\":[" << P.vl << "," << P.vr
+      << "],\"materialize\":" << (P.materialize ? "true" : "false") << "}";
+  }
+  o << "],\"streams\":[";
+  for (size_t j = 0; j < g.streams.size(); ++j) {
+    auto& S = g.streams[j];
+    o << (j ? "," : "") << "{\"src\":\"" << (S.src_is_stage ? p.stages[S.src].name : p.images[S.src].name)
+      << "\",\"plane_mode\":" << S.plane_mode << ",\"hi\":" << S.hi << ",\"lo\":" << S.lo << ",\"window\":" << S.depth
+      << ",\"smem_ext\":[" << S.xl << "," << S.xr << "]}";
+  }
+  int ng = 0;
+  for (auto& r : g.greads) ng += r.kind == RKind::GATHER;
+  o << "],\"gathers\":" << ng << "}";
+  return o.str();
+}
+
+// ------------------------------------------------------------------------------------------ paper mode
+std::string paper_analyze_group(const Analysis& A, const std::vector<int>& stages, const int T[3], const int B[3],
+                                double f, int tx, int regs_per_stage, const pmg_gpu_spec& S, const pmg_weights& w) {
+  const Pipeline& p = *A.p;
+  // paper dims (x, y, z) <- normalised (2, 1, 0)
+  const int pd[3] = {2, 1, 0};
+  std::array<int, 3> Bv{B[0], B[1], B[2]};
+  // pad the block to a multiple of WarpSize along x
+  int threads = B[0] * B[1] * B[2];
+  if (threads % S.warp_size) {
+    int x = B[0];
+    while ((x * B[1] * B[2]) % S.warp_size) ++x;
+    Bv[0] = x;
+  }
+  std::array<int, 3> W = warp_sizes(Bv, S.warp_size);
+  int wt[3] = {T[0] * W[0], T[1] * W[1], T[2] * W[2]};
+  int warps_per_dim[3] = {(Bv[0] + W[0] - 1) / W[0], (Bv[1] + W[1] - 1) / W[1], (Bv[2] + W[2] - 1) / W[2]};
+  // overlaps O_i^n: backward accumulation of left+right reach from the group's liveouts
+  const int n = (int)p.stages.size();
+  std::vector<char> in(n, 0);
+  for (int s : stages) in[s] = 1;
+  std::vector<std::array<int, 3>> L(n, {0, 0, 0}), Rr(n, {0, 0, 0});
+  std::vector<char> live(n, 0);
+  for (int s : stages) {
+    bool lo = std::find(p.liveouts.begin(), p.liveouts.end(), s) != p.liveouts.end();
+    for (int c : p.consumers[s])
+      if (!in[c]) lo = true;
+    live[s] = lo;
+  }
+  bool constant = true;
+  std::vector<int> order;
+  for (int s : p.topo)
+    if (in[s]) order.push_back(s);
+  for (int ii = (int)order.size() - 1; ii >= 0; --ii) {
+    int s = order[ii];
+    for (int c : p.consumers[s]) {
+      if (!in[c]) continue;
+      for (int ri : A.reads_of[c]) {
+        const ReadSite& r = A.reads[ri];
+        if (!r.src_is_stage || r.src != s) continue;
+        for (int d = 0; d < 3; ++d) {
+          int nd = pd[d];
+          int64_t off = 0;
+          if (r.form[nd] == Form::UNIT) off = r.off[nd];
+          else if (r.form[nd] != Form::ABSENT) constant = false;
+          L[s][d] = std::max(L[s][d], L[c][d] + (int)std::max<int64_t>(0, -off));
+          Rr[s][d] = std::max(Rr[s][d], Rr[c][d] + (int)std::max<int64_t>(0, off));
+        }
+      }
+    }
+  }
+  std::ostringstream o;
+  o.precision(12);
+  o << "{\"block\":[" << Bv[0] << "," << Bv[1] << "," << Bv[2] << "],\"warp\":[" << W[0] << "," << W[1] << "," << W[2]
+    << "],\"warp_tile\":[" << wt[0] << "," << wt[1] << "," << wt[2] << "],\"stages\":[";
+  double shmem_floats = 0, redundant = 0, computed = 0;
+  int buffers = 0;
+  for (size_t i = 0; i < order.size(); ++i) {
+    int s = order[i];
+    double pts = 1, useful = 1, spad = 1;
+    int O[3];
+    for (int d = 0; d < 3; ++d) {
+      O[d] = L[s][d] + Rr[s][d];
+      pts *= wt[d] + O[d];
+      useful *= wt[d];
+      spad *= warps_per_dim[d] * (wt[d] + O[d]);   // prod ceil(B_i/W_i)(T_i W_i + O_i^n)
+    }
+    o << (i ? "," : "") << "{\"stage\":\"" << p.stages[s].name << "\",\"overlap\":[" << O[0] << "," << O[1] << "," << O[2]
+      << "],\"scratchpad\":" << spad << ",\"liveout\":" << (live[s] ? "true" : "false") << "}";
+    if (!live[s]) {
+      shmem_floats += spad;
+      redundant += pts - useful;
+      computed += pts;
+      ++buffers;
+    }
+  }
+  o << "],\"overlap_numerator\":" << redundant << ",\"overlap_denominator\":" << computed << ",";
+  CostBreakdown c;
+  int64_t dims[3] = {A.stage_ext[order.back()].e[2], A.stage_ext[order.back()].e[1], A.stage_ext[order.back()].e[0]};
+  double total_threads = 1;
+  for (int d = 0; d < 3; ++d) total_threads *= std::ceil((double)dims[d] / T[d]);
+  int tb = Bv[0] * Bv[1] * Bv[2];
+  c.total_threads = total_threads;                                        // l.933
+  c.warps_per_tb = tb / (double)S.warp_size;                              // l.938
+  c.tb_per_sm = total_threads / tb / S.nsms;                              // l.939
+  c.sh_mem_per_tb = shmem_floats * 4.0;                                   // l.940-942 (bytes, f32 scratchpads)
+  c.sh_mem_per_tb *= (1.0 - f);                                           // l.943
+  int split = T[0] > 1 ? 0 : (T[1] > 1 ? 1 : 2);
+  c.reg_tile = std::round(T[split] * f) * std::max(1, buffers);           // l.944 (R13)
+  c.reg_per_th = c.reg_tile + (double)regs_per_stage * order.size();      // l.960
+  // global transactions: group-external loads, 32 lanes along x from the representative origin
+  double txs = 0;
+  for (int s : order)
+    for (int ri : A.reads_of[s]) {
+      const ReadSite& r = A.reads[ri];
+      if (r.src_is_stage && in[r.src]) continue;
+      int esz = dtype_size(r.src_is_stage ? p.stages[r.src].dtype : p.images[r.src].dtype);
+      int64_t off = r.form[2] == Form::UNIT ? r.off[2] : 0;
+      // iterations of the consumer's loop per warp tile (R14): its computed region / W
+      double iters = 1;
+      for (int d = 0; d < 3; ++d) iters *= std::ceil((double)(wt[d] + L[s][d] + Rr[s][d]) / W[d]);
+      txs += iters * min_txs((off - L[s][0]) * esz, (int64_t)W[0] * esz, tx);
+    }
+  c.total_gl_txs = txs;
+  double tile_vol = (double)wt[0] * wt[1] * wt[2];
+  c.txs_per_point = txs / tile_vol;
+  if (!constant) { c.infinite = true; c.why = "non-constant dependence vectors"; }
+  double tpi = 0;
+  for (int s : order) tpi += stage_ops(p, s) / S.sm_clock_hz;
+  alg2_tail(c, S, w, tile_vol, tpi, redundant, computed, tx);
+  o << "\"cost\":" << cost_json(c) << "}";
+  return o.str();
+}
+
+}  // namespace pmg

@@ -1,0 +1,49 @@
+// select.hpp — model-based fusion grouping and tile-size selection (§6).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/pmg.h"
+#include "plan.hpp"
+
+namespace pmg {
+
+struct CostBreakdown {          // every term of Alg. 2
+  double total_threads = 0, warps_per_tb = 0, tb_per_sm = 0;
+  double sh_mem_per_tb = 0;     // bytes (after the fracReg split, l.943)
+  double reg_tile = 0, reg_per_th = 0;
+  double total_gl_txs = 0;      // per warp tile (l.949-954)
+  double txs_per_point = 0;     // normalised per output point (reading R14)
+  double max_tb_per_sm = 0, sh_mem_occ = 0, reg_occ = 0, occupancy = 0;
+  double warp_bw = 0, mem_time = 0, compute_time = 0;
+  double unallocated_sh_mem = 0, unused_reg = 0, frac_overlap = 0, extra_tbs = 0;
+  double cost = 0;
+  bool infinite = false;
+  std::string why;
+};
+
+bool gpu_preset(const std::string& name, pmg_gpu_spec* out);
+bool weights_preset(const std::string& name, pmg_weights* out);
+
+// static per-stage profile (Alg. 2 inputs RegUsage(H), TimePerIter(H))
+double stage_ops(const Pipeline& p, int stage);
+
+// B200-mode Alg. 2 for a built group (KConfig -> paper symbols, DESIGN.md §"Selector")
+CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& spec, const pmg_weights& w);
+
+// argmin over the configuration space for one group; returns false if every point is infinite
+bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const pmg_gpu_spec& spec,
+                 const pmg_weights& w, const pmg_sched_opts& opts, CostBreakdown* cb);
+
+// DP fusion over convex groups (contiguous runs of the topological order), total = sum of group costs
+Schedule schedule(const Analysis& A, const pmg_gpu_spec& spec, const pmg_weights& w, const pmg_sched_opts& opts);
+
+// the paper's §4 geometry + Alg. 2 for an explicit group and (T, B, fracReg, txSz) — analysis pins
+std::string paper_analyze_group(const Analysis& A, const std::vector<int>& stages, const int T[3], const int B[3],
+                                double frac_reg, int tx_size, int regs_per_stage, const pmg_gpu_spec& spec,
+                                const pmg_weights& w);
+
+std::string cost_json(const CostBreakdown& c);
+std::string config_json(const Analysis& A, const Group& g);
+
+}  // namespace pmg

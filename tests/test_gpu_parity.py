@@ -1,0 +1,84 @@
+"""GPU parity: the CUDA path (through the C ABI) against the independent oracle, element by element, on
+seeded inputs at sizes spanning several warp tiles with ragged tails; schedule sweeps (the result must not
+depend on the schedule); edge shapes.  Bar: bit-exact (float results too, by construction — reading R3);
+the BASELINE.json tolerance (1e-4 abs on [0,1] outputs, 1e-5 range-relative for Harris) is the ceiling
+asserted."""
+import numpy as np
+import pytest
+
+import pmg_inputs as PI
+from gpu_util import compare, run_gpu
+from oracle import evaluate
+
+pytestmark = pytest.mark.gpu
+
+import paper_1909_07190_b200 as pmg  # noqa: E402
+
+TOL = {"blur": dict(float_tol=1e-4), "unsharp": dict(float_tol=1e-4), "harris": dict(rel_range=1e-5),
+       "local_laplacian": dict(float_tol=1e-4), "camera": {}}
+
+
+def check(name, W, H, opts=None, variant="uniform", bit_exact=True):
+    w = PI.small(name, W, H)
+    inp = w.inputs(variant)
+    exp = evaluate(w.text, w.params, inp)
+    got, plan = run_gpu(w.text, w.params, inp, opts=opts)
+    for k in exp:
+        neq, d = compare(got[k], exp[k], **TOL[name])
+        if bit_exact:
+            assert neq == 0, f"{name} {W}x{H}: {neq} elements differ from the oracle (max {d})"
+    return plan
+
+
+def test_fig1_shuffle_selftest():
+    """PAPER.md Fig. 1 (lines 252-260): lane 0 receives the warp sum 0+1+...+31 = 496."""
+    assert pmg.selftest_shuffle(0) == 496
+
+
+@pytest.mark.parametrize("W,H", [(128, 128), (1, 1), (33, 1), (127, 131), (4097, 3), (300, 257)])
+def test_blur_parity(W, H):
+    check("blur", W, H)
+
+
+@pytest.mark.parametrize("W,H", [(256, 200), (1000, 37), (64, 64), (5, 3)])
+def test_harris_parity(W, H):
+    check("harris", W, H)
+
+
+def test_harris_structured():
+    check("harris", 500, 300, variant="structured")
+
+
+@pytest.mark.parametrize("variant", ["uniform", "structured"])
+def test_unsharp_parity(variant):
+    check("unsharp", 300, 170, variant=variant)
+
+
+SWEEP = [dict(vec=v, chunks=tx, rows=th, warps=nw, prefetch=pf)
+         for (v, tx, th, nw, pf) in [(1, 1, 1, 1, 1), (2, 1, 3, 2, 2), (4, 1, 8, 4, 4), (4, 2, 32, 4, 2),
+                                     (2, 4, 5, 8, 3), (1, 2, 64, 2, 4), (4, 4, 16, 1, 1)]]
+
+
+@pytest.mark.parametrize("cfg", SWEEP, ids=lambda c: "V{vec}TX{chunks}TH{rows}NW{warps}P{prefetch}".format(**c))
+@pytest.mark.parametrize("name", ["blur", "harris", "unsharp"])
+def test_schedule_invariance(name, cfg):
+    """Any (tile, block, prefetch) configuration computes the same function."""
+    check(name, 211, 77, opts=pmg.sched_opts(**cfg, tx_size=32))
+
+
+@pytest.mark.parametrize("name", ["blur", "harris", "unsharp"])
+def test_unfused_equals_fused(name):
+    """One kernel per stage (every intermediate through HBM) == the fused group."""
+    check(name, 150, 90, opts=pmg.sched_opts(fuse=False))
+
+
+def test_camera_parity():
+    check("camera", 264, 130)
+
+
+def test_local_laplacian_small_parity():
+    w = PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005)
+    inp = w.inputs("structured")
+    exp = evaluate(w.text, w.params, inp)
+    got, _ = run_gpu(w.text, w.params, inp)
+    compare(got["out"], exp["out"], float_tol=1e-4)
