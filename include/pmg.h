@@ -113,7 +113,8 @@ typedef struct {
   int32_t tx_size;      /* 32 or 128 */
   int32_t budget;       /* max candidates per group (bounded search); <=0 = exhaustive */
   int32_t fuse;         /* 0 = one stage per group, 1 = DP fusion (default) */
-  int32_t reserved[7];
+  int32_t regcap;       /* registers per thread cap (__launch_bounds__ min-blocks); <=0 = automatic */
+  int32_t reserved[6];
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);

@@ -202,7 +202,8 @@ pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, cons
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
-    Schedule sch = schedule(A, S, W, o);
+    RegProbe probe = make_probe(A);
+    Schedule sch = schedule(A, S, W, o, &probe);
     return put_json(sch.json, json, cap, needed);
   })
 }
@@ -250,7 +251,8 @@ pmg_status pmg_emit(pmg_pipeline p, const int64_t* params, int nparams, const pm
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
-    Schedule sch = schedule(A, S, W, o);
+    RegProbe probe = make_probe(A);
+    Schedule sch = schedule(A, S, W, o, &probe);
     std::string out = "{\"schedule\":" + sch.json + ",\"groups\":[";
     for (size_t i = 0; i < sch.groups.size(); ++i) {
       std::string src = emit_group(A, sch.groups[i]);
@@ -280,7 +282,8 @@ pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, co
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
-    Schedule sch = schedule(A, S, W, o);
+    RegProbe probe = make_probe(A);
+    Schedule sch = schedule(A, S, W, o, &probe);
     std::string out = "{\"schedule\":" + sch.json + ",\"kernels\":[";
     for (size_t i = 0; i < sch.groups.size(); ++i) {
       Compiled c = jit_compile(sch.groups[i].name, emit_group(A, sch.groups[i]));

@@ -18,6 +18,7 @@
 //     rewrites are exact ones: x / 2^k -> x * 2^-k, and a + 2^k*b -> fma(2^k, b, a) (2^k*b exact).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -77,11 +78,74 @@ struct Emitter {
     if (g.U % depth == 0) return ((u - b) % depth + depth) % depth;
     return b;
   }
+  // ---- register storage of rows ----
+  // Unpaired buffers: one scalar per element e in [-el, V+er).  Paired buffers (float rows, V even):
+  // float2 q_j = (e_j, e_{j+V/2}) for j in [-el, V/2+er), so that packed FADD2/FMUL2/FFMA2 results feed
+  // packed consumers without register moves; element e lives canonically in q_e.x (e < V/2, incl. the
+  // left extension) or q_{e-V/2}.y (e >= V/2, incl. the right extension); extension pairs also carry a
+  // copy of one core element ("pair completion").
+  bool pair_on() const { return V >= 2 && V % 2 == 0 && pair_stride() > 0; }
+  bool st_paired(int i) const { return pair_on() && p.stages[g.gs[i].id].dtype == DType::F32; }
+  bool sr_paired(int j) const { return pair_on() && g.streams[j].dtype == DType::F32; }
+  std::string qname(char pre, int i, int sl, int k, int j) const {
+    return std::string(1, pre) + std::to_string(i) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_q" + ename(j);
+  }
+  std::string canon(char pre, int i, int sl, int k, int e) const {
+    const int h = V / 2;
+    if (e < h) return qname(pre, i, sl, k, e) + ".x";
+    return qname(pre, i, sl, k, e - h) + ".y";
+  }
   std::string sv(int i, int sl, int k, int e) const {
+    if (st_paired(i)) return canon('n', i, sl, k, e);
     return "n" + std::to_string(i) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_e" + ename(e);
   }
   std::string tv(int j, int sl, int k, int e) const {
+    if (sr_paired(j)) return canon('s', j, sl, k, e);
     return "s" + std::to_string(j) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_e" + ename(e);
+  }
+  // declare all slots of one buffer
+  void declare(char pre, int i, bool paired, bool isfloat, int depth, int el, int er) {
+    o << "    " << (paired ? "float2" : (isfloat ? "float" : "int")) << " ";
+    bool first = true;
+    for (int sl = 0; sl < depth; ++sl)
+      for (int kk = 0; kk < TX; ++kk) {
+        if (paired) {
+          for (int j = -el; j < V / 2 + er; ++j) {
+            o << (first ? "" : ", ") << qname(pre, i, sl, kk, j) << " = make_float2(0.f, 0.f)";
+            first = false;
+          }
+        } else {
+          for (int e = -el; e < V + er; ++e) {
+            o << (first ? "" : ", ") << (pre == 'n' ? sv(i, sl, kk, e) : tv(i, sl, kk, e)) << " = 0";
+            first = false;
+          }
+        }
+      }
+    o << ";\n";
+  }
+  // copy a whole row (all storage) from slot a to slot b
+  void copy_row(char pre, int i, bool paired, int el, int er, int a_, int b_, const std::string& ind) {
+    for (int kk = 0; kk < TX; ++kk) {
+      if (paired) {
+        for (int j = -el; j < V / 2 + er; ++j) o << ind << qname(pre, i, b_, kk, j) << " = " << qname(pre, i, a_, kk, j) << ";\n";
+      } else {
+        for (int e = -el; e < V + er; ++e)
+          o << ind << (pre == 'n' ? sv(i, b_, kk, e) : tv(i, b_, kk, e)) << " = " << (pre == 'n' ? sv(i, a_, kk, e) : tv(i, a_, kk, e)) << ";\n";
+      }
+    }
+  }
+  // fill the duplicated core element of every extension pair
+  void complete_pairs(char pre, int i, int sl, int el, int er, const std::string& ind) {
+    const int h = V / 2;
+    for (int kk = 0; kk < TX; ++kk) {
+      for (int j = -el; j < 0; ++j) {   // q_j = (e_j, e_{j+h}); e_{j+h} canonical elsewhere
+        std::string src = canon(pre, i, sl, kk, j + h);
+        o << ind << qname(pre, i, sl, kk, j) << ".y = " << src << ";\n";
+      }
+      for (int j = h; j < h + er; ++j) {  // q_j = (e_j, e_{j+h}): e_j is a core element
+        o << ind << qname(pre, i, sl, kk, j) << ".x = " << canon(pre, i, sl, kk, j) << ";\n";
+      }
+    }
   }
 
   // ---- expression emission (ctx: consumer stage pos i, chunk k, element v, sub-step u) ----
@@ -257,6 +321,79 @@ struct Emitter {
     return {"pmg_ldg<" + std::string(ctype(dt)) + ">(" + base + ", " + idx[2] + ")", dtype_is_float(dt) ? Kind::Float : Kind::Int};
   }
 
+  // ---- packed-pair evaluation: elements (va, vb) of one lane as one float2 expression tree ----
+  struct R2 { bool pair; std::string p; R a, b; };
+
+  std::string pack(const R2& r) { return r.pair ? r.p : "make_float2(" + tof(r.a).s + ", " + tof(r.b).s + ")"; }
+
+  bool pairable(const Expr& e) {
+    if (e.kind != Kind::Float) return false;
+    switch (e.op) {
+      case Expr::FLT: case Expr::ACCESS: return true;
+      case Expr::UN: return e.text == "-";
+      case Expr::BIN:
+        if (e.text == "+" || e.text == "-" || e.text == "*") return true;
+        if (e.text == "/" && e.args[1]->op == Expr::FLT) {
+          int k;
+          return is_pow2_float(e.args[1]->fval, &k) && std::isnormal(1.0f / e.args[1]->fval);
+        }
+        return false;
+      case Expr::CALL: return e.text == "lerp";
+      default: return false;
+    }
+  }
+
+  R2 ex2(const Expr& e, int i, int k, int va, int vb, int u) {
+    if (!pairable(e)) return R2{false, "", ex(e, Ctx{i, k, va, u}), ex(e, Ctx{i, k, vb, u})};
+    switch (e.op) {
+      case Expr::FLT: return R2{true, "pmg_bc2(" + flit(e.fval) + ")", {}, {}};
+      case Expr::ACCESS: {
+        int ri = site.at(&e);
+        const GRead& gr = g.greads.at(g.read_map.at(ri));
+        const GStage& C = g.gs[i];
+        if (vb == va + V / 2) {
+          if (gr.kind == RKind::STAGE && st_paired(gr.idx)) {
+            const GStage& P = g.gs[gr.idx];
+            return R2{true, qname('n', gr.idx, slot(P.depth, P.hi - C.hi - gr.dy, u), k, va + gr.dx), {}, {}};
+          }
+          if (gr.kind == RKind::STREAM && sr_paired(gr.idx)) {
+            const GStream& S = g.streams[gr.idx];
+            return R2{true, qname('s', gr.idx, slot(S.depth, S.hi - C.hi - gr.dy, u), k, va + gr.dx), {}, {}};
+          }
+        }
+        R a = ex(e, Ctx{i, k, va, u}), b = ex(e, Ctx{i, k, vb, u});
+        return R2{true, "make_float2(" + a.s + ", " + b.s + ")", {}, {}};
+      }
+      case Expr::UN: return R2{true, "pmg_neg2(" + pack(ex2(*e.args[0], i, k, va, vb, u)) + ")", {}, {}};
+      case Expr::CALL: {   // lerp(a, b, w) = a * (1 - w) + b * w
+        std::string a = pack(ex2(*e.args[0], i, k, va, vb, u)), b = pack(ex2(*e.args[1], i, k, va, vb, u)),
+                    w = pack(ex2(*e.args[2], i, k, va, vb, u));
+        return R2{true, "pmg_add2(pmg_mul2(" + a + ", pmg_sub2(pmg_bc2(1.0f), " + w + ")), pmg_mul2(" + b + ", " + w + "))", {}, {}};
+      }
+      default: break;
+    }
+    const std::string& op = e.text;
+    if (op == "+" || op == "-") {
+      const Expr* mb;
+      float m;
+      if (pow2_mul(*e.args[1], &mb, &m)) {
+        std::string a = pack(ex2(*e.args[0], i, k, va, vb, u)), b = pack(ex2(*mb, i, k, va, vb, u));
+        return R2{true, "pmg_fma2(pmg_bc2(" + flit(op == "+" ? m : -m) + "), " + b + ", " + a + ")", {}, {}};
+      }
+      if (pow2_mul(*e.args[0], &mb, &m)) {
+        std::string b = pack(ex2(*mb, i, k, va, vb, u)), a = pack(ex2(*e.args[1], i, k, va, vb, u));
+        return R2{true, "pmg_fma2(pmg_bc2(" + flit(m) + "), " + b + ", " + (op == "+" ? a : "pmg_neg2(" + a + ")") + ")", {}, {}};
+      }
+    }
+    std::string a = pack(ex2(*e.args[0], i, k, va, vb, u));
+    if (op == "/") {
+      return R2{true, "pmg_mul2(" + a + ", pmg_bc2(" + flit(1.0f / e.args[1]->fval) + "))", {}, {}};
+    }
+    std::string b = pack(ex2(*e.args[1], i, k, va, vb, u));
+    const char* f = op == "+" ? "pmg_add2" : op == "-" ? "pmg_sub2" : "pmg_mul2";
+    return R2{true, std::string(f) + "(" + a + ", " + b + ")", {}, {}};
+  }
+
   std::string conv_store(const R& v, DType dt) {
     if (dt == DType::F32) return tof(v).s;
     R i = toi(v);
@@ -269,81 +406,98 @@ struct Emitter {
   }
 
   // ---- kernel text ----
+  int himax = 0, xlm = 0, xrm = 0;
+
+  // packed-pair stride: pairs (v, v + stride) inside a lane's V elements; 0 = scalar
+  int pair_stride() const {
+    if (V < 2 || V % 2) return 0;
+    const char* e = getenv("PMG_PAIR_STRIDE");   // experimental packed-pair storage (off by default)
+    int m = e ? atoi(e) : 0;
+    if (m <= 0) return 0;
+    return m == 1 ? 1 : V / 2;
+  }
+
+  int phase_of(int t) const { return (((t - g.t_first) % g.U) + g.U) % g.U; }
+
   std::string run() {
     const KConfig& k = g.cfg;
     const int n = (int)g.gs.size();
     o << "// generated by libpmg (emit.cpp) for group " << g.name << ": ";
     for (auto& s : g.gs) o << p.stages[s.id].name << " ";
     o << "\n#include \"pmg_otpw.cuh\"\n\n";
+    for (auto& P : g.gs) himax = std::max(himax, P.hi);
+    for (auto& S : g.streams) himax = std::max(himax, S.hi);
+    for (auto& S : g.streams) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
     o << "#define V " << V << "\n#define TX " << TX << "\n#define CW " << g.CW << "\n#define PL " << g.PL
       << "\n#define OW " << g.OW << "\n#define TH " << k.TH << "\n#define NW " << k.NW << "\n#define PREF " << k.PREF
       << "\n#define TFIRST " << g.t_first << "\n#define NSTEPS " << g.nsteps << "\n#define USTEP " << g.U
       << "\n#define RING " << g.ring_bytes << "\n#define WSMEM " << g.warp_smem << "\n#define BARB "
-      << ((8 * k.PREF + 15) / 16 * 16) << "\n";
-    int xlm = 0, xrm = 0;
-    for (auto& S : g.streams) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
-    o << "#define XLM " << xlm << "\n#define XRM " << xrm << "\n\n";
+      << ((8 * k.PREF + 15) / 16 * 16) << "\n#define XLM " << xlm << "\n#define XRM " << xrm << "\n#define HIMAX " << himax
+      << "\n\n";
     int nt = std::max<int>(1, (int)g.tensors.size()), ntab = std::max<int>(1, (int)p.tables.size()),
         np = std::max<int>(1, (int)p.params.size());
     o << "struct PmgArgs {\n  PmgTensor t[" << nt << "];\n  const char* tab[" << ntab << "];\n  int tabn[" << ntab
       << "];\n  int prm[" << np << "];\n  int H, W, gy0, gy1, nty, ntx, npl, nfr, ntiles, pad_;\n};\n\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32) " << g.name << "(const __grid_constant__ PmgArgs a) {\n";
+    int minb = k.regcap > 0 ? std::max(1, 65536 / (k.regcap * 32 * k.NW)) : 1;
+    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << "(const __grid_constant__ PmgArgs a) {\n";
     o << "  extern __shared__ __align__(128) char pmg_smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
          "  const int wib = threadIdx.x >> 5;\n"
          "  char* wsm = pmg_smem + wib * WSMEM;\n"
          "  const u32 bar0 = pmg_smem_addr(wsm);\n"
          "  char* ring = wsm + BARB;\n"
-         "  (void)ring; (void)bar0;\n"
+         "  const u32 ring_addr = pmg_smem_addr(ring);\n"
+         "  (void)ring; (void)bar0; (void)ring_addr;\n"
          "  const int gw = blockIdx.x * NW + wib;\n"
          "  const int nwt = gridDim.x * NW;\n"
          "  if (gw >= a.ntiles) return;\n"
          "  const int H = a.H, W = a.W;\n"
          "  const int my_tiles = (a.ntiles - gw + nwt - 1) / nwt;\n";
-    bool has_streams = !g.streams.empty();
-    if (has_streams) {
+    const bool hs = !g.streams.empty();
+    if (hs) {
+      // ---- TMA producer state: one request per step, PREF steps ahead of the consumer; lane 0 issues ----
       o << "  if (lane == 0) {\n    for (int i = 0; i < PREF; ++i) pmg_mbar_init(bar0 + 8 * i, 1);\n    pmg_mbar_init_fence();\n  }\n"
            "  __syncwarp();\n"
-           "  const long long total_req = (long long)my_tiles * NSTEPS;\n"
-           "  long long q_issue = 0;\n  u32 phase = 0u;\n";
-      // request issue (lane 0)
-      o << "  auto issue = [&](long long q) {\n"
-           "    const int itq = (int)(q / NSTEPS), tq = TFIRST + (int)(q % NSTEPS);\n"
-           "    const int tile = gw + itq * nwt;\n"
+           "  const bool leader = lane == 0;\n"
+           "  int p_y0 = 0, pn_y0 = 0;\n  u32 p_total = 0, pn_total = 0;\n";
+      for (size_t j = 0; j < g.streams.size(); ++j)
+        o << "  const char* p_src" << j << " = nullptr; const char* pn_src" << j << " = nullptr; u32 p_dst" << j << " = 0, pn_dst" << j
+          << " = 0, p_bytes" << j << " = 0, pn_bytes" << j << " = 0;\n";
+      // tile -> request constants (divisions once per tile)
+      o << "  auto p_params = [&](int tile, int& y0r, u32& tot";
+      for (size_t j = 0; j < g.streams.size(); ++j) o << ", const char*& src" << j << ", u32& dst" << j << ", u32& byt" << j;
+      o << ") {\n"
            "    const int txq = tile % a.ntx, rq = tile / a.ntx, tyq = rq % a.nty, rq2 = rq / a.nty, pcq = rq2 % a.npl, frq = rq2 / a.npl;\n"
-           "    const int y0q = a.gy0 + tyq * TH, cxq = txq * OW - PL;\n"
-           "    const int sl = (int)(q % PREF);\n"
-           "    const u32 bar = bar0 + 8 * sl;\n"
-           "    char* dst = ring + sl * RING;\n"
-           "    u32 bytes = 0;\n"
-           "    (void)pcq; (void)frq;\n";
+           "    (void)pcq; (void)frq;\n"
+           "    y0r = a.gy0 + tyq * TH;\n"
+           "    const int cxq = txq * OW - PL;\n"
+           "    tot = 0;\n";
       for (size_t j = 0; j < g.streams.size(); ++j) {
         const GStream& S = g.streams[j];
-        const Ext3& se = S.src_is_stage ? A.stage_ext[S.src] : A.image_ext[S.src];
         int Aal = 16 / S.esz;
-        o << "    const PmgTensor& T" << j << " = a.t[" << S.tensor_slot << "];\n"
-          << "    const int row" << j << " = pmg_clampi(y0q + tq + (" << S.hi << "), 0, H - 1) - T" << j << ".row_base;\n"
-          << "    const int pl" << j << " = " << (S.plane_mode == 0 ? "0" : S.plane_mode == 1 ? "pcq" : std::to_string(S.plane_const)) << ";\n"
-          << "    const int xlo" << j << " = cxq - " << S.xl << ", xhi" << j << " = cxq + CW + " << S.xr << ";\n"
-          << "    const int clo" << j << " = xlo" << j << " < 0 ? 0 : xlo" << j << ";\n"
-          << "    const int wa" << j << " = (W + " << (Aal - 1) << ") / " << Aal << " * " << Aal << ";\n"
-          << "    const int chi" << j << " = xhi" << j << " > wa" << j << " ? wa" << j << " : xhi" << j << ";\n"
-          << "    bytes += (u32)(chi" << j << " - clo" << j << ") * " << S.esz << ";\n";
-        (void)se;
+        o << "    {\n      const PmgTensor& T = a.t[" << S.tensor_slot << "];\n"
+          << "      const int pl = " << (S.plane_mode == 0 ? "0" : S.plane_mode == 1 ? "pcq" : std::to_string(S.plane_const)) << ";\n"
+          << "      const int xlo = cxq - " << S.xl << ", xhi = cxq + CW + " << S.xr << ";\n"
+          << "      const int wa = (W + " << (Aal - 1) << ") / " << Aal << " * " << Aal << ";\n"
+          << "      const int clo = xlo < 0 ? 0 : xlo, chi = xhi > wa ? wa : xhi;\n"
+          << "      src" << j << " = T.ptr + (i64)frq * T.frame_stride + (i64)pl * T.plane_pitch - (i64)T.row_base * T.row_pitch + (i64)clo * " << S.esz << ";\n"
+          << "      dst" << j << " = " << S.smem_off << " + (u32)(clo - xlo) * " << S.esz << ";\n"
+          << "      byt" << j << " = (u32)(chi - clo) * " << S.esz << ";\n"
+          << "      tot += byt" << j << ";\n    }\n";
       }
-      o << "    pmg_mbar_expect_tx(bar, bytes);\n";
-      for (size_t j = 0; j < g.streams.size(); ++j) {
-        const GStream& S = g.streams[j];
-        o << "    pmg_bulk_g2s(pmg_smem_addr(dst + " << S.smem_off << " + (clo" << j << " - xlo" << j << ") * " << S.esz
-          << "), T" << j << ".ptr + (i64)frq * T" << j << ".frame_stride + (i64)pl" << j << " * T" << j << ".plane_pitch + (i64)row" << j << " * T" << j
-          << ".row_pitch + (i64)clo" << j << " * " << S.esz << ", (u32)(chi" << j << " - clo" << j << ") * " << S.esz
-          << ", bar);\n";
-      }
-      o << "  };\n"
-           "  if (lane == 0) {\n    for (; q_issue < total_req && q_issue < PREF; ++q_issue) issue(q_issue);\n  }\n"
-           "  long long q_cons = 0;\n";
+      o << "  };\n";
+      o << "  p_params(gw, p_y0, p_total";
+      for (size_t j = 0; j < g.streams.size(); ++j) o << ", p_src" << j << ", p_dst" << j << ", p_bytes" << j;
+      o << ");\n";
+      // prologue: the first PREF requests of the first tile
+      o << "  for (int s = 0; s < PREF; ++s) {\n"
+           "    const u32 bar = bar0 + 8 * s;\n"
+           "    pmg_mbar_expect_tx_if(bar, p_total, leader);\n";
+      for (size_t j = 0; j < g.streams.size(); ++j)
+        o << "    pmg_bulk_g2s_if(ring_addr + s * RING + p_dst" << j << ", p_src" << j << " + (i64)pmg_clampi(p_y0 + (TFIRST + "
+          << g.streams[j].hi << ") + s, 0, H - 1) * a.t[" << g.streams[j].tensor_slot << "].row_pitch, p_bytes" << j << ", bar, leader);\n";
+      o << "  }\n  int c_slot = 0;\n  u32 phase = 0u;\n";
     }
-    // register declarations
     o << "  for (int it = 0; it < my_tiles; ++it) {\n"
          "    const int tile = gw + it * nwt;\n"
          "    const int tx = tile % a.ntx, rr = tile / a.ntx, ty = rr % a.nty, rr2 = rr / a.nty, pc = rr2 % a.npl, fr = rr2 / a.npl;\n"
@@ -352,122 +506,273 @@ struct Emitter {
          "    const int xL = cx + V * lane;\n"
          "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W);\n"
          "    const int yend = (y0 + TH < a.gy1) ? (y0 + TH) : a.gy1;\n"
+         "    const bool interior = !xb && (y0 + TFIRST >= 0) && (y0 + TH + HIMAX <= H) && (y0 + TH <= a.gy1);\n"
          "    (void)pc; (void)fr; (void)xL; (void)xb; (void)yend;\n";
+    if (hs) {
+      o << "    const bool has_next = it + 1 < my_tiles;\n"
+           "    if (has_next) p_params(tile + nwt, pn_y0, pn_total";
+      for (size_t j = 0; j < g.streams.size(); ++j) o << ", pn_src" << j << ", pn_dst" << j << ", pn_bytes" << j;
+      o << ");\n";
+    }
     for (int i = 0; i < n; ++i) {
       const GStage& P = g.gs[i];
-      int nslot = P.depth;
-      o << "    " << rtype(p.stages[P.id].dtype) << " ";
-      bool first = true;
-      for (int sl = 0; sl < nslot; ++sl)
-        for (int kk = 0; kk < TX; ++kk)
-          for (int e = -P.el; e < V + P.er; ++e) {
-            o << (first ? "" : ", ") << sv(i, sl, kk, e) << " = 0";
-            first = false;
-          }
-      o << ";\n";
+      if (!P.materialize) continue;
+      std::string T = "a.t[" + std::to_string(P.tensor_slot) + "]";
+      o << "    char* obase" << i << " = (char*)" << T << ".ptr + (i64)fr * " << T << ".frame_stride + (i64)pc * " << T
+        << ".plane_pitch - (i64)" << T << ".row_base * " << T << ".row_pitch + (i64)xL * " << dtype_size(p.stages[P.id].dtype)
+        << ";\n";
+    }
+    for (int i = 0; i < n; ++i) {
+      const GStage& P = g.gs[i];
+      declare('n', i, st_paired(i), p.stages[P.id].dtype == DType::F32, P.depth, P.el, P.er);
     }
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
-      o << "    " << rtype(S.dtype) << " ";
-      bool first = true;
-      for (int sl = 0; sl < S.depth; ++sl)
-        for (int kk = 0; kk < TX; ++kk)
-          for (int e = -S.el; e < V + S.er; ++e) {
-            o << (first ? "" : ", ") << tv((int)j, sl, kk, e) << " = 0";
-            first = false;
-          }
-      o << ";\n";
+      declare('s', (int)j, sr_paired((int)j), S.dtype == DType::F32, S.depth, S.el, S.er);
     }
-    o << "    for (int tb = TFIRST; tb < TH; tb += USTEP) {\n";
-    for (int u = 0; u < g.U; ++u) step(u);
-    o << "    }\n  }\n}\n";
+    // ---- interior tiles: branch-free bodies (warm-up unrolled, main loop, tail) ----
+    o << "    if (interior) {\n";
+    if (hs) {
+      for (size_t j = 0; j < g.streams.size(); ++j)
+        o << "      const char* q_ptr" << j << " = p_src" << j << " + (i64)(p_y0 + (TFIRST + " << g.streams[j].hi
+          << " + PREF)) * a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
+    }
+    for (int t = g.t_first; t < 0; ++t) {
+      int s_ = t - g.t_first + k.PREF;
+      step(true, phase_of(t), true, t, s_ < g.nsteps ? 1 : 0);
+    }
+    // main section: the refill of every step targets this tile (pointer increment, no clamp)
+    const int a_end = std::max(0, k.TH - k.PREF) / g.U * g.U;
+    if (a_end > 0) {
+      o << "      for (int tb = 0; tb < " << a_end << "; tb += USTEP) {\n";
+      for (int u = 0; u < g.U; ++u) {
+        o << "      { const int t = tb + " << u << ";\n";
+        step(true, phase_of(u), false, 0, 1);
+        o << "      }\n";
+      }
+      o << "      }\n";
+    }
+    if (a_end < k.TH) {
+      // tail: the refills cross into the next tile (selects, clamped rows)
+      o << "      for (int tb = " << a_end << "; tb < TH; tb += USTEP) {\n";
+      for (int u = 0; u < g.U; ++u) {
+        o << "      { const int t = tb + " << u << ";\n      if (t < TH) {\n";
+        step(true, phase_of(u), false, 0, 0);
+        o << "      }\n      }\n";
+      }
+      o << "      }\n";
+    }
+    // ---- border tiles: general bodies (clamped reads, edge replication, row checks) ----
+    o << "    } else {\n      for (int tb = TFIRST; tb < TH; tb += USTEP) {\n";
+    for (int u = 0; u < g.U; ++u) {
+      o << "      { const int t = tb + " << u << ";\n      if (t < TH) {\n";
+      step(false, u, false, 0, 0);
+      o << "      }\n      }\n";
+    }
+    o << "      }\n    }\n";
+    if (hs) {
+      o << "    p_y0 = pn_y0; p_total = pn_total;\n";
+      for (size_t j = 0; j < g.streams.size(); ++j)
+        o << "    p_src" << j << " = pn_src" << j << "; p_dst" << j << " = pn_dst" << j << "; p_bytes" << j << " = pn_bytes" << j << ";\n";
+    }
+    o << "  }\n}\n";
     return o.str();
   }
 
-  void shift_window(bool stage, int i, int depth, int el, int er) {
+  void shift_window(bool stage, int i, int depth, int el, int er, const std::string& ind) {
     // shift-mode window (depth does not divide the unroll factor): r{b} = r{b-1}
-    for (int b = depth - 1; b >= 1; --b)
-      for (int kk = 0; kk < TX; ++kk)
-        for (int e = -el; e < V + er; ++e)
-          o << "        " << (stage ? sv(i, b, kk, e) : tv(i, b, kk, e)) << " = " << (stage ? sv(i, b - 1, kk, e) : tv(i, b - 1, kk, e)) << ";\n";
+    bool paired = stage ? st_paired(i) : sr_paired(i);
+    for (int b = depth - 1; b >= 1; --b) copy_row(stage ? 'n' : 's', i, paired, el, er, b - 1, b, ind);
   }
 
-  void step(int u) {
-    const int n = (int)g.gs.size();
-    o << "      { // sub-step " << u << "\n      const int t = tb + " << u << ";\n      if (t < TH) {\n";
-    // ---- group inputs: wait for the ring slot, read this step's rows (type (2): shared memory) ----
-    if (!g.streams.empty()) {
-      o << "        const int slq = (int)(q_cons % PREF);\n"
-           "        pmg_mbar_wait(bar0 + 8 * slq, (phase >> slq) & 1u);\n"
-           "        phase ^= 1u << slq;\n"
-           "        const char* srow = ring + slq * RING;\n";
-      for (size_t j = 0; j < g.streams.size(); ++j) {
-        const GStream& S = g.streams[j];
-        bool rot = S.depth <= 1 || g.U % S.depth == 0;
-        if (!rot) shift_window(false, (int)j, S.depth, S.el, S.er);
-        int sl = rot ? slot(S.depth, 0, u) : 0;
-        std::string ct = ctype(S.dtype);
-        o << "        {\n          const char* sb = srow + " << S.smem_off << ";\n"
-          << "          if (!xb) {\n";
-        // aligned vector reads covering [-el, V+er) per chunk
-        int lo = -S.el, hi = V + S.er;
-        int vlo = (int)std::floor((double)lo / V) * V, vhi = (int)std::ceil((double)hi / V) * V;
-        for (int kk = 0; kk < TX; ++kk)
-          for (int vb = vlo; vb < vhi; vb += V) {
-            o << "            { " << ct << " w[" << V << "]; pmg_lds_vec<" << ct << ", " << V << ">(sb + (" << S.xl << " + "
-              << 32 * V * kk << " + V * lane + (" << vb << ")) * " << S.esz << ", w);";
-            for (int q = 0; q < V; ++q)
-              if (vb + q >= lo && vb + q < hi) o << " " << tv((int)j, sl, kk, vb + q) << " = PmgElem<" << ct << ">::cv(w[" << q << "]);";
-            o << " }\n";
-          }
-        o << "          } else {\n"
-          << "            const int xo = cx - " << S.xl << ";\n";
+  void stream_reads(int u, bool fast, const std::string& ind) {
+    o << ind << "const int slq = c_slot;\n"
+      << ind << "pmg_mbar_wait(bar0 + 8 * slq, (phase >> slq) & 1u);\n"
+      << ind << "phase ^= 1u << slq;\n"
+      << ind << "c_slot = (slq + 1 == PREF) ? 0 : slq + 1;\n"
+      << ind << "{\n" << ind << "const char* srow = ring + slq * RING;\n";
+    for (size_t j = 0; j < g.streams.size(); ++j) {
+      const GStream& S = g.streams[j];
+      bool rot = S.depth <= 1 || g.U % S.depth == 0;
+      if (!rot) shift_window(false, (int)j, S.depth, S.el, S.er, ind);
+      int sl = rot ? slot(S.depth, 0, u) : 0;
+      std::string ct = ctype(S.dtype);
+      int lo = -S.el, hi = V + S.er;
+      int vlo = (int)std::floor((double)lo / V) * V, vhi = (int)std::ceil((double)hi / V) * V;
+      o << ind << "{\n" << ind << "  const char* sb = srow + " << S.smem_off << ";\n";
+      if (!fast) o << ind << "  if (!xb) {\n";
+      for (int kk = 0; kk < TX; ++kk)
+        for (int vb = vlo; vb < vhi; vb += V) {
+          o << ind << "    { " << ct << " w[" << V << "]; pmg_lds_vec<" << ct << ", " << V << ">(sb + (" << S.xl << " + "
+            << 32 * V * kk << " + V * lane + (" << vb << ")) * " << S.esz << ", w);";
+          for (int q = 0; q < V; ++q)
+            if (vb + q >= lo && vb + q < hi) o << " " << tv((int)j, sl, kk, vb + q) << " = PmgElem<" << ct << ">::cv(w[" << q << "]);";
+          o << " }\n";
+        }
+      if (!fast) {
+        o << ind << "  } else {\n" << ind << "    const int xo = cx - " << S.xl << ";\n";
         for (int kk = 0; kk < TX; ++kk)
           for (int e = lo; e < hi; ++e)
-            o << "            " << tv((int)j, sl, kk, e) << " = pmg_lds<" << ct << ">(sb, pmg_clampi(xL + " << 32 * V * kk + e
+            o << ind << "    " << tv((int)j, sl, kk, e) << " = pmg_lds<" << ct << ">(sb, pmg_clampi(xL + " << 32 * V * kk + e
               << ", 0, W - 1) - xo);\n";
-        o << "          }\n        }\n";
+        o << ind << "  }\n";
       }
-      o << "        __syncwarp();\n"
-           "        if (lane == 0 && q_issue < total_req) { pmg_fence_proxy_async(); issue(q_issue); ++q_issue; }\n"
-           "        ++q_cons;\n";
+      if (sr_paired((int)j)) complete_pairs('s', (int)j, sl, S.el, S.er, ind + "  ");
+      o << ind << "}\n";
     }
-    // ---- stages in topological order ----
+    o << ind << "}\n" << ind << "__syncwarp();\n";
+  }
+
+  // refill the slot read in this step with the request PREF steps ahead (next tile when it crosses NSTEPS)
+  void refill(bool tconst, int tval, int rmode, const std::string& ind) {
+    std::string tt = tconst ? std::to_string(tval) : "t";
+    if (rmode == 1) {
+      // same tile, interior: rows need no clamp; the source pointers advance one row per step
+      o << ind << "{\n" << ind << "  const u32 bar = bar0 + 8 * slq;\n"
+        << ind << "  pmg_fence_proxy_async_if(leader);\n"
+        << ind << "  pmg_mbar_expect_tx_if(bar, p_total, leader);\n";
+      for (size_t j = 0; j < g.streams.size(); ++j) {
+        const GStream& S = g.streams[j];
+        o << ind << "  pmg_bulk_g2s_if(ring_addr + slq * RING + p_dst" << j << ", q_ptr" << j << ", p_bytes" << j << ", bar, leader);\n"
+          << ind << "  q_ptr" << j << " += a.t[" << S.tensor_slot << "].row_pitch;\n";
+      }
+      o << ind << "}\n";
+      return;
+    }
+    o << ind << "{\n";
+    if (tconst) {
+      int s = tval - g.t_first + g.cfg.PREF;
+      bool nx = s >= g.nsteps;
+      int sr = nx ? s - g.nsteps : s;
+      o << ind << "  const bool nx = " << (nx ? "true" : "false") << ";\n" << ind << "  const int sr = " << sr << ";\n";
+    } else {
+      o << ind << "  const int s = " << tt << " - TFIRST + PREF;\n"
+        << ind << "  const bool nx = s >= NSTEPS;\n"
+        << ind << "  const int sr = nx ? s - NSTEPS : s;\n";
+    }
+    o << ind << "  const bool go = leader && (!nx || has_next);\n"
+      << ind << "  const u32 bar = bar0 + 8 * slq;\n"
+      << ind << "  const int yq = nx ? pn_y0 : p_y0;\n"
+      << ind << "  pmg_fence_proxy_async_if(go);\n"
+      << ind << "  pmg_mbar_expect_tx_if(bar, nx ? pn_total : p_total, go);\n";
+    for (size_t j = 0; j < g.streams.size(); ++j) {
+      const GStream& S = g.streams[j];
+      o << ind << "  pmg_bulk_g2s_if(ring_addr + slq * RING + (nx ? pn_dst" << j << " : p_dst" << j << "), (nx ? pn_src" << j
+        << " : p_src" << j << ") + (i64)pmg_clampi(yq + (TFIRST + " << S.hi << ") + sr, 0, H - 1) * a.t[" << S.tensor_slot
+        << "].row_pitch, nx ? pn_bytes" << j << " : p_bytes" << j << ", bar, go);\n";
+    }
+    o << ind << "}\n";
+  }
+
+  void store(int i, int cur, bool fast, bool tconst, int tval, const std::string& ind) {
+    const GStage& P = g.gs[i];
+    DType dt = p.stages[P.id].dtype;
+    std::string ct = ctype(dt);
+    int esz = dtype_size(dt);
+    std::string rowv = "row" + std::to_string(i);
+    if (fast && tconst) {
+      int r = tval + P.hi;
+      if (r < 0 || r >= g.cfg.TH) return;   // another tile's row
+    }
+    bool check_rows = !fast || (!tconst && P.hi > 0);
+    o << ind << "{\n";
+    if (check_rows) o << ind << "if (" << rowv << " >= y0 && " << rowv << " < yend) {\n";
+    o << ind << "  char* orow = obase" << i << " + (i64)" << rowv << " * a.t[" << P.tensor_slot << "].row_pitch;\n";
+    if (!fast)
+      o << ind << "  const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
+        << ind << "  const int oxhi = (cx + PL + OW) < W ? (cx + PL + OW) : W;\n";
+    for (int kk = 0; kk < TX; ++kk) {
+      std::string dst = "orow + " + std::to_string(32 * V * kk * esz);
+      if (fast) {
+        // interior tile: the output lanes of each chunk are compile-time constants
+        int lo = g.PL - 32 * V * kk <= 0 ? 0 : std::min(32, (g.PL - 32 * V * kk) / V);
+        int hi = std::max(0, std::min(32, (g.CW - g.PR - 32 * V * kk) / V));
+        if (hi <= lo) continue;
+        o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
+        for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
+        o << "};\n";
+        std::string cond = (lo == 0 && hi == 32) ? "" : "if (lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi) + ") ";
+        o << ind << "    " << cond << "pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n" << ind << "  }\n";
+      } else {
+        o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
+        for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
+        o << "};\n";
+        o << ind << "    const int xs = xL + " << 32 * V * kk << ";\n"
+          << ind << "    if (xs >= oxlo && xs + V <= oxhi) pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n"
+          << ind << "    else if (xs < oxhi && xs + V > oxlo) {\n";
+        for (int v = 0; v < V; ++v)
+          o << ind << "      if (xs + " << v << " >= oxlo && xs + " << v << " < oxhi) reinterpret_cast<" << ct << "*>(" << dst
+            << ")[" << v << "] = w[" << v << "];\n";
+        o << ind << "    }\n" << ind << "  }\n";
+      }
+    }
+    if (check_rows) o << ind << "}\n";
+    o << ind << "}\n";
+  }
+
+  // one step of the wavefront: fast = interior tile (no row/column checks); tconst = t known at emit time
+  void step(bool fast, int u, bool tconst, int tval, int rmode) {
+    const int n = (int)g.gs.size();
+    const std::string ind = "        ";
+    o << ind << "{ // " << (fast ? "interior" : "general") << " step" << (tconst ? " t=" + std::to_string(tval) : "") << " phase "
+      << u << "\n";
+    if (tconst) o << ind << "const int t = " << tval << ";\n";
+    if (!g.streams.empty()) stream_reads(u, fast, ind);
     for (int i = 0; i < n; ++i) {
       const GStage& P = g.gs[i];
       const StageDecl& sd = p.stages[P.id];
+      if (tconst && tval < P.lo - P.hi) continue;   // not active yet (warm-up)
       bool rot = P.depth <= 1 || g.U % P.depth == 0;
       int cur = rot ? slot(P.depth, 0, u) : 0;
       int prev = rot ? slot(P.depth, 1, u) : 1;
-      o << "        // stage " << sd.name << " (hi " << P.hi << ", lo " << P.lo << ", window " << P.depth << ")\n"
-        << "        if (t >= " << (P.lo - P.hi) << ") {\n"
-        << "          const int row" << i << " = y0 + t + (" << P.hi << ");\n";
-      if (!rot) shift_window(true, i, P.depth, P.el, P.er);
-      o << "          if (row" << i << " >= 0 && row" << i << " < H) {\n";
-      for (int kk = 0; kk < TX; ++kk)
-        for (int v = 0; v < V; ++v) {
-          R val = ex(*sd.expr, Ctx{i, kk, v, u});
-          o << "            " << sv(i, cur, kk, v) << " = " << conv_store(val, sd.dtype) << ";\n";
-        }
-      if (P.xfix) {
+      std::string rowv = "row" + std::to_string(i);
+      o << ind << "// stage " << sd.name << " (hi " << P.hi << ", lo " << P.lo << ", window " << P.depth << ")\n";
+      std::string in2 = ind;
+      if (!fast) {
+        o << ind << "if (t >= " << (P.lo - P.hi) << ") {\n";
+        in2 = ind + "  ";
+      } else {
+        o << ind << "{\n";
+      }
+      o << in2 << "const int " << rowv << " = y0 + t + (" << P.hi << ");\n" << in2 << "(void)" << rowv << ";\n";
+      if (!rot) shift_window(true, i, P.depth, P.el, P.er, in2);
+      std::string in3 = in2;
+      if (!fast) {
+        o << in2 << "if (" << rowv << " >= 0 && " << rowv << " < H) {\n";
+        in3 = in2 + "  ";
+      }
+      if (st_paired(i) && pairable(*sd.expr)) {
+        for (int kk = 0; kk < TX; ++kk)
+          for (int v = 0; v < V / 2; ++v) {
+            R2 r = ex2(*sd.expr, i, kk, v, v + V / 2, u);
+            o << in3 << qname('n', i, cur, kk, v) << " = " << pack(r) << ";\n";
+          }
+      } else {
+        for (int kk = 0; kk < TX; ++kk)
+          for (int v = 0; v < V; ++v) {
+            R val = ex(*sd.expr, Ctx{i, kk, v, u});
+            o << in3 << sv(i, cur, kk, v) << " = " << conv_store(val, sd.dtype) << ";\n";
+          }
+      }
+      if (P.xfix && !fast) {
         // border tiles: columns outside [0, W) take the edge value (reading R1)
-        o << "            if (xb) {\n";
+        o << in3 << "if (xb) {\n";
         for (int side = 0; side < 2; ++side) {
-          o << "              {\n                const int off = " << (side == 0 ? "-cx" : "W - 1 - cx") << ";\n"
-            << "                if (" << (side == 0 ? "cx < 0" : "cx + CW > W") << ") {\n"
-            << "                  const int kq = off / (32 * V), lq = (off % (32 * V)) / V, eq = off % V;\n"
-            << "                  " << rtype(sd.dtype) << " sel = " << sv(i, cur, 0, 0) << ";\n";
+          o << in3 << "  if (" << (side == 0 ? "cx < 0" : "cx + CW > W") << ") {\n"
+            << in3 << "    const int off = " << (side == 0 ? "-cx" : "W - 1 - cx") << ";\n"
+            << in3 << "    const int kq = off / (32 * V), lq = (off % (32 * V)) / V, eq = off % V;\n"
+            << in3 << "    " << rtype(sd.dtype) << " sel = " << sv(i, cur, 0, 0) << ";\n";
           for (int kk = 0; kk < TX; ++kk)
             for (int v = 0; v < V; ++v)
-              o << "                  if (kq == " << kk << " && eq == " << v << ") sel = " << sv(i, cur, kk, v) << ";\n";
-          o << "                  const " << rtype(sd.dtype) << " edge = pmg_shfl(sel, lq);\n";
+              o << in3 << "    if (kq == " << kk << " && eq == " << v << ") sel = " << sv(i, cur, kk, v) << ";\n";
+          o << in3 << "    const " << rtype(sd.dtype) << " edge = pmg_shfl(sel, lq);\n";
           for (int kk = 0; kk < TX; ++kk)
             for (int v = 0; v < V; ++v)
-              o << "                  if (xL + " << 32 * V * kk + v << (side == 0 ? " < 0" : " > W - 1") << ") " << sv(i, cur, kk, v)
+              o << in3 << "    if (xL + " << 32 * V * kk + v << (side == 0 ? " < 0" : " > W - 1") << ") " << sv(i, cur, kk, v)
                 << " = edge;\n";
-          o << "                }\n              }\n";
+          o << in3 << "  }\n";
         }
-        o << "            }\n";
+        o << in3 << "}\n";
       }
       // extension elements: neighbour lanes / neighbour chunks (load types (3) and (4))
       for (int kk = 0; kk < TX; ++kk) {
@@ -475,55 +780,31 @@ struct Emitter {
           int q = (int)std::floor((double)e / V), ee = e - q * V;
           std::string own = sv(i, cur, kk, ee);
           std::string send = kk > 0 ? "(lane >= " + std::to_string(32 + q) + " ? " + sv(i, cur, kk - 1, ee) + " : " + own + ")" : own;
-          o << "            " << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + (" << q << ")) & 31);\n";
+          o << in3 << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + (" << q << ")) & 31);\n";
         }
         for (int e = V; e < V + P.er; ++e) {
           int q = e / V, ee = e - q * V;
           std::string own = sv(i, cur, kk, ee);
           std::string send = kk + 1 < TX ? "(lane < " + std::to_string(q) + " ? " + sv(i, cur, kk + 1, ee) + " : " + own + ")" : own;
-          o << "            " << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + " << q << ") & 31);\n";
+          o << in3 << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + " << q << ") & 31);\n";
         }
       }
-      if (P.depth > 1) {
-        // first real row of a top-border tile: rows < 0 replicate row 0
-        o << "            if (row" << i << " == 0) {\n";
-        for (int sl = 0; sl < P.depth; ++sl) {
-          if (sl == cur) continue;
-          for (int kk = 0; kk < TX; ++kk)
-            for (int e = -P.el; e < V + P.er; ++e) o << "              " << sv(i, sl, kk, e) << " = " << sv(i, cur, kk, e) << ";\n";
+      if (st_paired(i)) complete_pairs('n', i, cur, P.el, P.er, in3);
+      if (!fast) {
+        if (P.depth > 1) {
+          o << in3 << "if (" << rowv << " == 0) {\n";
+          for (int sl = 0; sl < P.depth; ++sl)
+            if (sl != cur) copy_row('n', i, st_paired(i), P.el, P.er, cur, sl, in3 + "  ");
+          o << in3 << "}\n" << in2 << "} else if (" << rowv << " >= H) {\n";
+          copy_row('n', i, st_paired(i), P.el, P.er, prev, cur, in3);
         }
-        o << "            }\n";
-        o << "          } else if (row" << i << " >= H) {\n";
-        for (int kk = 0; kk < TX; ++kk)
-          for (int e = -P.el; e < V + P.er; ++e) o << "            " << sv(i, cur, kk, e) << " = " << sv(i, prev, kk, e) << ";\n";
+        o << in2 << "}\n";
       }
-      o << "          }\n";
-      if (P.materialize) {
-        DType dt = sd.dtype;
-        std::string ct = ctype(dt);
-        o << "          if (row" << i << " >= y0 && row" << i << " < yend) {\n"
-          << "            const PmgTensor& O = a.t[" << P.tensor_slot << "];\n"
-          << "            char* orow = (char*)O.ptr + (i64)fr * O.frame_stride + (i64)pc * O.plane_pitch + (i64)(row" << i << " - O.row_base) * O.row_pitch;\n"
-          << "            const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
-          << "            const int oxhi = (cx + PL + OW) < W ? (cx + PL + OW) : W;\n";
-        for (int kk = 0; kk < TX; ++kk) {
-          o << "            {\n              const int xs = xL + " << 32 * V * kk << ";\n"
-            << "              " << ct << " w[" << V << "] = {";
-          for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
-          o << "};\n"
-            << "              if (xs >= oxlo && xs + V <= oxhi) pmg_stg_vec<" << ct << ", " << V << ">(orow + (i64)xs * " << dtype_size(dt)
-            << ", w);\n"
-            << "              else {\n";
-          for (int v = 0; v < V; ++v)
-            o << "                if (xs + " << v << " >= oxlo && xs + " << v << " < oxhi) reinterpret_cast<" << ct
-              << "*>(orow)[xs + " << v << "] = w[" << v << "];\n";
-          o << "              }\n            }\n";
-        }
-        o << "          }\n";
-      }
-      o << "        }\n";
+      if (P.materialize) store(i, cur, fast, tconst, tval, in2);
+      o << ind << "}\n";
     }
-    o << "      }\n      }\n";
+    if (!g.streams.empty()) refill(tconst, tval, rmode, ind);
+    o << ind << "}\n";
   }
 };
 

@@ -202,6 +202,7 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   for (auto& P : g.gs) g.t_first = std::min(g.t_first, P.lo - P.hi);
   for (auto& st : g.streams) g.t_first = std::min(g.t_first, st.lo - st.hi);
   g.nsteps = k.TH - g.t_first;
+  if (!g.streams.empty() && k.PREF > g.nsteps) return bad("prefetch depth exceeds the steps of one tile");
   // unroll factor for register-window rotation
   int U = 1;
   auto lcm = [](int a, int b) { return a / std::gcd(a, b) * b; };
@@ -228,10 +229,12 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   g.npl = g.ext.has[0] ? g.ext.e[0] : 1;
   g.ntx = (g.ext.e[2] + g.OW - 1) / g.OW;
   // register estimate (selector input; refined by ptxas when compiled)
-  int regs = 24;
-  for (auto& P : g.gs) regs += P.depth * k.TX * (k.V + P.el + P.er);
-  for (auto& st : g.streams) regs += st.depth * k.TX * (k.V + st.el + st.er);
-  g.regs_est = regs;
+  // register estimate: windows (+60% for temporaries / scheduling), fitted to ptxas counts on B200;
+  // the selector replaces it with the real count for its finalists (compile probe)
+  int win = 0;
+  for (auto& P : g.gs) win += P.depth * k.TX * (k.V + P.el + P.er);
+  for (auto& st : g.streams) win += st.depth * k.TX * (k.V + st.el + st.er);
+  g.regs_est = 40 + (win * 8 + 4) / 5;
   g.why_infeasible.clear();
   return true;
 }

@@ -36,6 +36,14 @@ __device__ __forceinline__ float pmg_div(float a, float b) { return __fdiv_rn(a,
 __device__ __forceinline__ float pmg_sqrt(float a) { return __fsqrt_rn(a); }
 // a + (m * b) where m = 2^k (k >= 0): m*b is exact, so one rounding == the written two roundings
 __device__ __forceinline__ float pmg_fma_exact(float m, float b, float a) { return __fmaf_rn(m, b, a); }
+// packed pairs (sm_100a FADD2 / FMUL2 / FFMA2): two elements per instruction, each rounded exactly as
+// its scalar counterpart (a - b == a + (-b) exactly in IEEE 754)
+__device__ __forceinline__ float2 pmg_add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 pmg_sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 pmg_mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 pmg_fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 pmg_neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 pmg_bc2(float c) { return make_float2(c, c); }
 __device__ __forceinline__ float pmg_fmin(float a, float b) { return (b < a) ? b : a; }
 __device__ __forceinline__ float pmg_fmax(float a, float b) { return (b > a) ? b : a; }
 __device__ __forceinline__ float pmg_i2f(int a) { return __int2float_rn(a); }
@@ -147,6 +155,19 @@ __device__ __forceinline__ void pmg_mbar_wait(u32 bar, u32 phase) {
 __device__ __forceinline__ void pmg_bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+// predicated variants: every lane executes the instruction stream (no divergence), only `p` lanes act
+__device__ __forceinline__ void pmg_mbar_expect_tx_if(u32 bar, u32 bytes, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+               "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar), "r"(bytes), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void pmg_bulk_g2s_if(u32 dst, const void* src, u32 bytes, u32 bar, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+               "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void pmg_fence_proxy_async_if(bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q fence.proxy.async.shared::cta;\n}" ::"r"((int)p) : "memory");
 }
 __device__ __forceinline__ void pmg_fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -126,6 +126,18 @@ Compiled jit_compile(const std::string& name, const std::string& source) {
   return c;
 }
 
+RegProbe make_probe(const Analysis& A) {
+  return [&A](const Group& g, int* regs, int* spill) {
+    if (g.regs_est <= 96) return false;   // far from the register limit: the estimate is enough
+    Group h = g;
+    h.name = "pmg_probe";
+    Compiled c = jit_compile(h.name, emit_group(A, h));
+    *regs = c.regs;
+    *spill = std::max(c.spill_stores, 0) + std::max(c.spill_loads, 0);
+    return c.regs > 0;
+  };
+}
+
 // -------------------------------------------------------------------------------------------- plans
 static void check(CUresult r, const char* what) {
   if (r != CUDA_SUCCESS) throw Error(-6, std::string(what) + ": " + cu_err(r));
@@ -174,7 +186,8 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     o.smem_chunks = -1;
     o.fuse = 1;
   }
-  P->sch = schedule(P->A, P->spec, P->weights, o);
+  RegProbe probe = make_probe(P->A);
+  P->sch = schedule(P->A, P->spec, P->weights, o, &probe);
   const Pipeline& pp = *p;
   P->nimages = (int)pp.images.size();
   P->ntables = (int)pp.tables.size();

@@ -62,4 +62,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
 
 std::string kernel_dir();   // directory of libpmg.so (for the cubin cache)
 
+// compile probe for the selector (ptxas register / spill counts of a candidate)
+RegProbe make_probe(const Analysis& A);
+
 }  // namespace pmg

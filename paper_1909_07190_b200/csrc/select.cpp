@@ -171,17 +171,16 @@ static bool feasible_stage_set(const Analysis& A, const std::vector<int>& stages
 }
 
 bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const pmg_gpu_spec& S, const pmg_weights& w,
-                 const pmg_sched_opts& o, CostBreakdown* out) {
+                 const pmg_sched_opts& o, CostBreakdown* out, const RegProbe* probe) {
   std::vector<int> Vs = o.vec > 0 ? std::vector<int>{o.vec} : std::vector<int>{1, 2, 4};
   std::vector<int> TXs = o.chunks > 0 ? std::vector<int>{o.chunks} : std::vector<int>{1, 2, 4};
-  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 32, 64};
-  std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{2, 4, 8};
-  std::vector<int> PFs = o.prefetch > 0 ? std::vector<int>{o.prefetch} : std::vector<int>{2, 4};
+  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 64};
+  std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{1, 2, 4, 8};
+  std::vector<int> PFs = o.prefetch > 0 ? std::vector<int>{o.prefetch} : std::vector<int>{4, 8};
   std::vector<int> TXSZ = o.tx_size > 0 ? std::vector<int>{o.tx_size} : std::vector<int>{32, 128};
   std::vector<int> Ss = o.smem_chunks >= 0 ? std::vector<int>{o.smem_chunks} : std::vector<int>{0};
-  bool found = false;
-  Group best;
-  CostBreakdown bc;
+  struct Cand { Group g; CostBreakdown c; };
+  std::vector<Cand> cands;
   std::string why = "no candidate";
   long count = 0;
   for (int V : Vs)
@@ -192,31 +191,55 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
             for (int PF : PFs)
               for (int tx : TXSZ) {
                 if (o.budget > 0 && count >= o.budget) break;
+                if (S_ > TX) continue;
                 Group cand;
                 cand.stages = g.stages;
-                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx};
-                if (S_ > TX) continue;
+                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0};
                 ++count;
                 if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
                 CostBreakdown c = b200_cost(A, cand, S, w);
                 if (c.infinite) { why = c.why; continue; }
-                auto vol = [](const KConfig& q) { return (double)q.V * q.TX * q.TH; };
-                bool better = !found || c.cost < bc.cost - 1e-12 ||
-                              (std::fabs(c.cost - bc.cost) <= 1e-12 &&     // tie-break
-                               (vol(cand.cfg) < vol(best.cfg) ||
-                                (vol(cand.cfg) == vol(best.cfg) &&
-                                 (cand.cfg.NW < best.cfg.NW ||
-                                  (cand.cfg.NW == best.cfg.NW && (cand.cfg.S > best.cfg.S ||
-                                                                  (cand.cfg.S == best.cfg.S && cand.cfg.tx_size > best.cfg.tx_size)))))));
-                if (better) { best = cand; bc = c; found = true; }
+                cands.push_back({cand, c});
               }
-  if (!found) { g.why_infeasible = why; return false; }
-  g = best;
-  if (out) *out = bc;
+  if (cands.empty()) { g.why_infeasible = why; return false; }
+  // tie-break: smaller tile volume, smaller block, larger fracReg, larger txSz
+  auto better = [](const Cand& a, const Cand& b) {
+    if (std::fabs(a.c.cost - b.c.cost) > 1e-12) return a.c.cost < b.c.cost;
+    auto vol = [](const KConfig& q) { return (double)q.V * q.TX * q.TH; };
+    if (vol(a.g.cfg) != vol(b.g.cfg)) return vol(a.g.cfg) < vol(b.g.cfg);
+    if (a.g.cfg.NW != b.g.cfg.NW) return a.g.cfg.NW < b.g.cfg.NW;
+    if (a.g.cfg.S != b.g.cfg.S) return a.g.cfg.S < b.g.cfg.S;
+    return a.g.cfg.tx_size > b.g.cfg.tx_size;
+  };
+  std::sort(cands.begin(), cands.end(), better);
+  // finalists: replace the register estimate by ptxas' count (RegUsage "measured with nvcc");
+  // spilling configurations are rejected (their registers exceed MaxRegPerTh)
+  if (probe && *probe) {
+    const size_t K = std::min<size_t>(cands.size(), 4);
+    std::vector<Cand> fin;
+    for (size_t i = 0; i < cands.size() && fin.size() < K; ++i) {
+      Cand c = cands[i];
+      int regs = -1, spill = -1;
+      if (!(*probe)(c.g, &regs, &spill) || regs <= 0) { fin.push_back(c); continue; }
+      c.g.regs_est = regs;
+      c.c = b200_cost(A, c.g, S, w);
+      if (spill > 0) { c.c.infinite = true; c.c.why = "register spills"; c.c.cost = std::numeric_limits<double>::infinity(); }
+      fin.push_back(c);
+    }
+    std::sort(fin.begin(), fin.end(), better);
+    if (!fin.empty() && !fin[0].c.infinite) {
+      g = fin[0].g;
+      if (out) *out = fin[0].c;
+      return true;
+    }
+  }
+  g = cands[0].g;
+  if (out) *out = cands[0].c;
   return true;
 }
 
-Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w, const pmg_sched_opts& o) {
+Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w, const pmg_sched_opts& o,
+                  const RegProbe* probe) {
   const Pipeline& p = *A.p;
   const int n = (int)p.stages.size();
   Schedule sch;
@@ -237,7 +260,7 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
       for (int s : p.topo)
         if (gos[s] == seen[gi]) g.stages.push_back(s);
       CostBreakdown cb;
-      if (!best_config(A, g, gos, S, w, o, &cb))
+      if (!best_config(A, g, gos, S, w, o, &cb, probe))
         throw Error(PMG_ERR_INFEASIBLE, "group " + std::to_string(gi) + ": " + g.why_infeasible);
       g.name = "pmg_g" + std::to_string(gi);
       js << (gi ? "," : "") << "{\"config\":" << config_json(A, g) << ",\"cost\":" << cost_json(cb) << "}";
@@ -288,13 +311,13 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
   js << "{\"mode\":\"dp\",\"total_cost\":" << best[n] << ",\"groups\":[";
   for (size_t gi = 0; gi < segs.size(); ++gi) {
     Group g = seg_group[segs[gi].first][segs[gi].second];
-    // rebuild with the final grouping (materialisation depends on the other groups)
+    // re-select with the final grouping (materialisation depends on the other groups) and with the
+    // register probe for the finalists
     Group h;
     h.stages = g.stages;
-    h.cfg = g.cfg;
-    if (!build_group(A, h, sch.group_of_stage)) throw Error(PMG_ERR_INFEASIBLE, h.why_infeasible);
+    CostBreakdown cb;
+    if (!best_config(A, h, sch.group_of_stage, S, w, o, &cb, probe)) throw Error(PMG_ERR_INFEASIBLE, h.why_infeasible);
     h.name = "pmg_g" + std::to_string(gi);
-    CostBreakdown cb = b200_cost(A, h, S, w);
     js << (gi ? "," : "") << "{\"config\":" << config_json(A, h) << ",\"cost\":" << cost_json(cb) << "}";
     sch.groups.push_back(h);
   }

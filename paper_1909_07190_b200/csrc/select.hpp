@@ -1,5 +1,6 @@
 // select.hpp — model-based fusion grouping and tile-size selection (§6).
 #pragma once
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -31,12 +32,16 @@ double stage_ops(const Pipeline& p, int stage);
 // B200-mode Alg. 2 for a built group (KConfig -> paper symbols, DESIGN.md §"Selector")
 CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& spec, const pmg_weights& w);
 
+// RegUsage(H) "measured with nvcc": compile a candidate and return ptxas' registers / spill bytes
+using RegProbe = std::function<bool(const Group& g, int* regs, int* spill_bytes)>;
+
 // argmin over the configuration space for one group; returns false if every point is infinite
 bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const pmg_gpu_spec& spec,
-                 const pmg_weights& w, const pmg_sched_opts& opts, CostBreakdown* cb);
+                 const pmg_weights& w, const pmg_sched_opts& opts, CostBreakdown* cb, const RegProbe* probe = nullptr);
 
 // DP fusion over convex groups (contiguous runs of the topological order), total = sum of group costs
-Schedule schedule(const Analysis& A, const pmg_gpu_spec& spec, const pmg_weights& w, const pmg_sched_opts& opts);
+Schedule schedule(const Analysis& A, const pmg_gpu_spec& spec, const pmg_weights& w, const pmg_sched_opts& opts,
+                  const RegProbe* probe = nullptr);
 
 // the paper's §4 geometry + Alg. 2 for an explicit group and (T, B, fracReg, txSz) — analysis pins
 std::string paper_analyze_group(const Analysis& A, const std::vector<int>& stages, const int T[3], const int B[3],
