@@ -114,7 +114,8 @@ typedef struct {
   int32_t budget;       /* max candidates per group (bounded search); <=0 = exhaustive */
   int32_t fuse;         /* 0 = one stage per group, 1 = DP fusion (default) */
   int32_t regcap;       /* registers per thread cap (__launch_bounds__ min-blocks); <=0 = automatic */
-  int32_t reserved[6];
+  int32_t probe;        /* 1 = compile the selector's finalists to read ptxas register counts (default) */
+  int32_t reserved[5];
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);
@@ -179,6 +180,10 @@ pmg_status pmg_run_batch(pmg_plan plan, int nframes, const pmg_buf* in, const in
  * of the pipeline's full-resolution row space (parameter H). */
 pmg_status pmg_band_rows(pmg_plan plan, int band, int nbands, int64_t* out_r0, int64_t* out_r1, int64_t* in_r0,
                          int64_t* in_r1);
+/* the same band geometry without a GPU (schedule computed on the host with spec/weights/opts) */
+pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                              const pmg_weights* w, const pmg_sched_opts* opts, int band, int nbands, int64_t* out_r0,
+                              int64_t* out_r1, int64_t* in_r0, int64_t* in_r1);
 /* in[i] points at global row in_r0 of image i (tables: whole table); out[j] at global row out_r0 */
 pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, int nin, const pmg_buf* out,
                         int nout, void* workspace, void* stream);

@@ -60,7 +60,7 @@ class SchedOpts(C.Structure):
     _fields_ = [("group_of_stage", C.POINTER(C.c_int32)), ("vec", C.c_int32), ("chunks", C.c_int32),
                 ("smem_chunks", C.c_int32), ("rows", C.c_int32), ("warps", C.c_int32), ("prefetch", C.c_int32),
                 ("tx_size", C.c_int32), ("budget", C.c_int32), ("fuse", C.c_int32), ("regcap", C.c_int32),
-                ("reserved", C.c_int32 * 6)]
+                ("probe", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
 P = C.c_void_p
@@ -100,6 +100,8 @@ _sig = {
     "pmg_run_batch": (C.c_int, [P, C.c_int, C.POINTER(Buf), I64P, C.c_int, C.POINTER(Buf), I64P, C.c_int,
                                 C.c_void_p, C.c_void_p]),
     "pmg_band_rows": (C.c_int, [P, C.c_int, C.c_int, I64P, I64P, I64P, I64P]),
+    "pmg_band_rows_host": (C.c_int, [P, I64P, C.c_int, C.POINTER(GpuSpec), C.POINTER(Weights), C.POINTER(SchedOpts),
+                                     C.c_int, C.c_int, I64P, I64P, I64P, I64P]),
     "pmg_run_band": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.c_void_p,
                                C.c_void_p]),
     "pmg_selftest_shuffle": (C.c_int, [C.c_int, C.POINTER(C.c_int32)]),

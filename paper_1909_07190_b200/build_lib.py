@@ -1,7 +1,7 @@
 """Builds paper_1909_07190_b200/libpmg.so (host C++17 + NVRTC; device code is compiled for sm_100a by NVRTC
 at plan time from the hand-written csrc/kernels/pmg_otpw.cuh plus the emitted stage bodies).
 
-    python -m paper_1909_07190_b200.build_lib          # or __graft_entry__.build()
+    python paper_1909_07190_b200/build_lib.py          # or __graft_entry__.build()
 """
 from __future__ import annotations
 

@@ -182,6 +182,7 @@ void pmg_sched_opts_default(pmg_sched_opts* o) {
   o->smem_chunks = -1;
   o->budget = 0;
   o->fuse = 1;
+  o->probe = 1;
 }
 
 static void spec_or_default(const pmg_gpu_spec* s, const pmg_weights* w, pmg_gpu_spec& S, pmg_weights& W) {
@@ -203,7 +204,7 @@ pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, cons
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
     RegProbe probe = make_probe(A);
-    Schedule sch = schedule(A, S, W, o, &probe);
+    Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     return put_json(sch.json, json, cap, needed);
   })
 }
@@ -252,7 +253,7 @@ pmg_status pmg_emit(pmg_pipeline p, const int64_t* params, int nparams, const pm
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
     RegProbe probe = make_probe(A);
-    Schedule sch = schedule(A, S, W, o, &probe);
+    Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     std::string out = "{\"schedule\":" + sch.json + ",\"groups\":[";
     for (size_t i = 0; i < sch.groups.size(); ++i) {
       std::string src = emit_group(A, sch.groups[i]);
@@ -283,7 +284,7 @@ pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, co
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
     RegProbe probe = make_probe(A);
-    Schedule sch = schedule(A, S, W, o, &probe);
+    Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     std::string out = "{\"schedule\":" + sch.json + ",\"kernels\":[";
     for (size_t i = 0; i < sch.groups.size(); ++i) {
       Compiled c = jit_compile(sch.groups[i].name, emit_group(A, sch.groups[i]));
@@ -347,6 +348,30 @@ pmg_status pmg_band_rows(pmg_plan plan, int band, int nbands, int64_t* out_r0, i
   if (!plan || nbands < 1 || band < 0 || band >= nbands) return fail(PMG_ERR_ARG, "bad band");
   PMG_TRY({
     BandRows b = band_rows(*plan->plan, band, nbands);
+    if (out_r0) *out_r0 = b.out_r0;
+    if (out_r1) *out_r1 = b.out_r1;
+    if (in_r0) *in_r0 = b.in_r0;
+    if (in_r1) *in_r1 = b.in_r1;
+    return PMG_OK;
+  })
+}
+
+pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                              const pmg_weights* w, const pmg_sched_opts* opts, int band, int nbands, int64_t* out_r0,
+                              int64_t* out_r1, int64_t* in_r0, int64_t* in_r1) {
+  if (!p || nbands < 1 || band < 0 || band >= nbands) return fail(PMG_ERR_ARG, "bad band");
+  PMG_TRY({
+    Plan P;
+    P.pipe = p->p;
+    P.A = analyze(*p->p, pvec(params, nparams));
+    pmg_gpu_spec S;
+    pmg_weights W;
+    spec_or_default(spec, w, S, W);
+    pmg_sched_opts o;
+    if (opts) o = *opts;
+    else pmg_sched_opts_default(&o);
+    P.sch = schedule(P.A, S, W, o, nullptr);
+    BandRows b = band_rows(P, band, nbands);
     if (out_r0) *out_r0 = b.out_r0;
     if (out_r1) *out_r1 = b.out_r1;
     if (in_r0) *in_r0 = b.in_r0;

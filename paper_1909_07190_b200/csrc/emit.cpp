@@ -675,8 +675,11 @@ struct Emitter {
       if (r < 0 || r >= g.cfg.TH) return;   // another tile's row
     }
     bool check_rows = !fast || (!tconst && P.hi > 0);
+    std::string T = "a.t[" + std::to_string(P.tensor_slot) + "]";
+    std::string inbuf = "(unsigned)(" + rowv + " - " + T + ".row_base) < (unsigned)" + T + ".nrows";
     o << ind << "{\n";
-    if (check_rows) o << ind << "if (" << rowv << " >= y0 && " << rowv << " < yend) {\n";
+    if (check_rows) o << ind << "if (" << rowv << " >= y0 && " << rowv << " < yend && " << inbuf << ") {\n";
+    else o << ind << "if (" << inbuf << ") {\n";
     o << ind << "  char* orow = obase" << i << " + (i64)" << rowv << " * a.t[" << P.tensor_slot << "].row_pitch;\n";
     if (!fast)
       o << ind << "  const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
@@ -706,7 +709,7 @@ struct Emitter {
         o << ind << "    }\n" << ind << "  }\n";
       }
     }
-    if (check_rows) o << ind << "}\n";
+    o << ind << "}\n";
     o << ind << "}\n";
   }
 

@@ -25,7 +25,7 @@ struct PmgTensor {           // one planar [c][y][x] device tensor (40 bytes; mi
   i64 plane_pitch;           // bytes
   i64 frame_stride;          // bytes between batch frames (0 for tables / single images)
   int row_base;              // global row index of buffer row 0 (bands)
-  int pad;
+  int nrows;                 // rows present in the buffer: stores outside [row_base, row_base + nrows) are dropped
 };
 
 // ------------------------------------------------------------------ float semantics (reading R3)

@@ -185,9 +185,10 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     o.vec = o.chunks = o.rows = o.warps = o.prefetch = o.tx_size = -1;
     o.smem_chunks = -1;
     o.fuse = 1;
+    o.probe = 1;
   }
   RegProbe probe = make_probe(P->A);
-  P->sch = schedule(P->A, P->spec, P->weights, o, &probe);
+  P->sch = schedule(P->A, P->spec, P->weights, o, o.probe ? &probe : nullptr);
   const Pipeline& pp = *p;
   P->nimages = (int)pp.images.size();
   P->ntables = (int)pp.tables.size();
@@ -248,7 +249,7 @@ void plan_destroy(Plan* P) {
 
 // ---------------------------------------------------------------------------------- band geometry
 // rows needed of every stage / image for liveout rows [r0, r1) (cumulative halo, clipped)
-struct Need { std::vector<RowIv> stage, image; };
+struct Need { std::vector<RowIv> stage, image, group; };
 
 static Need rows_for(const Plan& P, int64_t r0, int64_t r1) {
   const Pipeline& p = *P.pipe;
@@ -273,11 +274,15 @@ static Need rows_for(const Plan& P, int64_t r0, int64_t r1) {
       else hull(n.image[r.src], need);
     }
   }
-  // group granularity: every stage of a group computes the group's row range
+  // group granularity: a group's kernel produces the hull of its materialised stages' rows (its in-group
+  // stages' halo rows are produced inside the tiles); every materialised stage of the group gets that range
   for (auto& g : P.sch.groups) {
     RowIv h{0, 0};
-    for (auto& s : g.gs) hull(h, n.stage[s.id]);
-    for (auto& s : g.gs) n.stage[s.id] = h;
+    for (auto& s : g.gs)
+      if (s.materialize) hull(h, n.stage[s.id]);
+    for (auto& s : g.gs)
+      if (s.materialize) n.stage[s.id] = h;
+    n.group.push_back(h);
   }
   return n;
 }
@@ -304,7 +309,7 @@ BandRows band_rows(const Plan& P, int band, int nbands) {
 
 // ------------------------------------------------------------------------------------------ launch
 #pragma pack(push, 1)
-struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, pad; };
+struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, nrows; };
 #pragma pack(pop)
 static_assert(sizeof(HostTensor) == 40, "PmgTensor mirror");
 
@@ -362,6 +367,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
         t.pp = in[id].plane_pitch_bytes;
         t.fs = in_fs ? in_fs[id] : 0;
         t.row_base = (int32_t)(banded ? in_row_base : 0);
+        t.nrows = (int32_t)(banded ? band_rows(P, band, nbands).in_r1 - in_row_base : A.image_ext[id].e[1]);
       } else {
         auto lit = std::find(p.liveouts.begin(), p.liveouts.end(), id);
         if (lit != p.liveouts.end()) {
@@ -371,6 +377,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
           t.pp = out[oi].plane_pitch_bytes;
           t.fs = out_fs ? out_fs[oi] : 0;
           t.row_base = (int32_t)(banded ? r0 : 0);
+          t.nrows = (int32_t)(banded ? r1 - r0 : A.stage_ext[id].e[1]);
         } else {
           const WsTensor* w = nullptr;
           for (auto& x : P.ws)
@@ -381,6 +388,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
           t.pp = w->plane_pitch;
           t.fs = (int64_t)P.ws_bytes;
           t.row_base = (int32_t)(banded ? need.stage[id].lo : 0);
+          t.nrows = (int32_t)(banded ? need.stage[id].hi - need.stage[id].lo : A.stage_ext[id].e[1]);
         }
       }
       std::memcpy(buf.data() + 40 * ti, &t, 40);
@@ -398,7 +406,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     int32_t Hg = (int32_t)g.ext.e[1], Wg = (int32_t)g.ext.e[2];
     int32_t gy0 = 0, gy1 = Hg;
     if (banded) {
-      RowIv h = need.stage[g.gs[0].id];
+      RowIv h = need.group[gi];
       gy0 = (int32_t)h.lo;
       gy1 = (int32_t)h.hi;
     }

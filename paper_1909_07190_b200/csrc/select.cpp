@@ -254,6 +254,7 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
       if (std::find(seen.begin(), seen.end(), gos[s]) == seen.end()) seen.push_back(gos[s]);
     sch.group_of_stage = gos;
     std::ostringstream js;
+    double total = 0;
     js << "{\"mode\":\"manual\",\"groups\":[";
     for (size_t gi = 0; gi < seen.size(); ++gi) {
       Group g;
@@ -264,9 +265,10 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
         throw Error(PMG_ERR_INFEASIBLE, "group " + std::to_string(gi) + ": " + g.why_infeasible);
       g.name = "pmg_g" + std::to_string(gi);
       js << (gi ? "," : "") << "{\"config\":" << config_json(A, g) << ",\"cost\":" << cost_json(cb) << "}";
+      total += cb.cost;
       sch.groups.push_back(g);
     }
-    js << "]}";
+    js << "],\"total_cost\":" << total << "}";
     sch.json = js.str();
     name_groups(sch);
     return sch;

@@ -42,7 +42,7 @@ def weights(name: str = "b200") -> B.Weights:
 
 
 def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, warps=-1, prefetch=-1, tx_size=-1,
-               budget=0, fuse=True, regcap=0) -> B.SchedOpts:
+               budget=0, fuse=True, regcap=0, probe=True) -> B.SchedOpts:
     o = B.SchedOpts()
     B.lib.pmg_sched_opts_default(C.byref(o))
     o.vec, o.chunks, o.smem_chunks, o.rows, o.warps, o.prefetch, o.tx_size = (
@@ -50,6 +50,7 @@ def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, 
     o.budget = budget
     o.fuse = 1 if fuse else 0
     o.regcap = regcap
+    o.probe = 1 if probe else 0
     if group_of_stage is not None:
         arr = (C.c_int32 * len(group_of_stage))(*group_of_stage)
         o._keep = arr                      # keep the array alive with the struct
@@ -130,6 +131,14 @@ class Pipeline:
         b = (C.c_int32 * 3)(*block)
         return B.call_json(B.lib.pmg_analyze_group, self._h, arr, n, ",".join(stages).encode(), t, b, float(frac_reg),
                            tx_size, regs_per_stage, _ref(spec), _ref(weights_))
+
+    def band_rows(self, params: dict, band: int, nbands: int, spec=None, weights_=None, opts=None):
+        """(out_r0, out_r1, in_r0, in_r1) of row band `band` of `nbands` (host-only geometry)."""
+        arr, n = self.param_values(params)
+        v = [C.c_int64() for _ in range(4)]
+        B.check(B.lib.pmg_band_rows_host(self._h, arr, n, _ref(spec), _ref(weights_), _ref(opts), band, nbands,
+                                         *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
 
     def emit(self, params: dict, spec=None, weights_=None, opts=None) -> dict:
         arr, n = self.param_values(params)
