@@ -142,6 +142,21 @@ Analysis analyze(const Pipeline& p, const std::vector<int64_t>& params) {
   return A;
 }
 
+// algorithmic operation count of an expression as written (roofline numerator)
+static int alg_ops(const Expr& e) {
+  int c = 0;
+  if (e.op == Expr::ACCESS) return 0;   // index expressions are coordinates, not the stage's arithmetic
+  for (auto& a : e.args) c += alg_ops(*a);
+  switch (e.op) {
+    case Expr::BIN: case Expr::UN: return c + 1;
+    case Expr::CALL:
+      if (e.text == "lerp") return c + 3;
+      if (e.text == "clamp" || e.text == "absd") return c + 2;
+      return c + 1;
+    default: return c;
+  }
+}
+
 std::string describe_pipeline(const Analysis& A) {
   const Pipeline& p = *A.p;
   std::ostringstream o;
@@ -149,7 +164,8 @@ std::string describe_pipeline(const Analysis& A) {
   for (size_t s = 0; s < p.stages.size(); ++s) {
     auto& e = A.stage_ext[s];
     o << (s ? "," : "") << "{\"name\":\"" << p.stages[s].name << "\",\"dtype\":\"" << dtype_name(p.stages[s].dtype)
-      << "\",\"extent\":[" << e.e[0] << "," << e.e[1] << "," << e.e[2] << "],\"ndim\":" << p.stages[s].vars.size() << "}";
+      << "\",\"extent\":[" << e.e[0] << "," << e.e[1] << "," << e.e[2] << "],\"ndim\":" << p.stages[s].vars.size()
+      << ",\"ops\":" << alg_ops(*p.stages[s].expr) << "}";
   }
   o << "],\"topo\":[";
   for (size_t i = 0; i < p.topo.size(); ++i) o << (i ? "," : "") << "\"" << p.stages[p.topo[i]].name << "\"";
