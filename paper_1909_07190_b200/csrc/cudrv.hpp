@@ -35,6 +35,12 @@ struct Drv {
   CUresult (*MemAlloc)(CUdeviceptr*, size_t);
   CUresult (*MemFree)(CUdeviceptr);
   CUresult (*MemcpyDtoH)(void*, CUdeviceptr, size_t);
+  CUresult (*StreamCreate)(CUstream*, unsigned);
+  CUresult (*StreamDestroy)(CUstream);
+  CUresult (*EventCreate)(CUevent*, unsigned);
+  CUresult (*EventDestroy)(CUevent);
+  CUresult (*EventRecord)(CUevent, CUstream);
+  CUresult (*StreamWaitEvent)(CUstream, CUevent, unsigned);
 };
 
 inline Drv& drv() {
@@ -73,6 +79,12 @@ inline Drv& drv() {
     PMG_SYM(MemAlloc, "cuMemAlloc_v2");
     PMG_SYM(MemFree, "cuMemFree_v2");
     PMG_SYM(MemcpyDtoH, "cuMemcpyDtoH_v2");
+    PMG_SYM(StreamCreate, "cuStreamCreate");
+    PMG_SYM(StreamDestroy, "cuStreamDestroy_v2");
+    PMG_SYM(EventCreate, "cuEventCreate");
+    PMG_SYM(EventDestroy, "cuEventDestroy_v2");
+    PMG_SYM(EventRecord, "cuEventRecord");
+    PMG_SYM(StreamWaitEvent, "cuStreamWaitEvent");
 #undef PMG_SYM
     if (!all) { d.err = "CUDA driver is missing required symbols"; return; }
     CUresult r = d.Init(0);

@@ -72,10 +72,18 @@ struct Emitter {
     for (size_t i = 0; i < A.reads.size(); ++i) site[A.reads[i].node] = (int)i;
   }
 
+  // per-kernel window depths and unroll factor (the interior kernel folds sums row by row and needs
+  // shallower windows than the border kernel)
+  std::vector<int> dS, dT;
+  int Uk = 1;
+  int back_shift = 0;   // set while emitting a fold segment evaluated m steps ahead of its stage row
+  int depS(int i) const { return dS.empty() ? g.gs[i].depth : dS[i]; }
+  int depT(int j) const { return dT.empty() ? g.streams[j].depth : dT[j]; }
+
   // physical window slot of back index b at sub-step u (rotation when depth | U, else shift naming)
   int slot(int depth, int b, int u) const {
     if (depth <= 1) return 0;
-    if (g.U % depth == 0) return ((u - b) % depth + depth) % depth;
+    if (Uk % depth == 0) return ((u - b) % depth + depth) % depth;
     return b;
   }
   // ---- register storage of rows ----
@@ -297,12 +305,14 @@ struct Emitter {
       const GStage& P = g.gs[gr.idx];
       int b = P.hi - C.hi - gr.dy;
       DType dt = p.stages[P.id].dtype;
-      return {sv(gr.idx, slot(P.depth, b, c.u), c.k, c.v + gr.dx), dtype_is_float(dt) ? Kind::Float : Kind::Int};
+      b -= back_shift;
+      return {sv(gr.idx, slot(depS(gr.idx), b, c.u), c.k, c.v + gr.dx), dtype_is_float(dt) ? Kind::Float : Kind::Int};
     }
     if (gr.kind == RKind::STREAM) {
       const GStream& S = g.streams[gr.idx];
       int b = S.hi - C.hi - gr.dy;
-      return {tv(gr.idx, slot(S.depth, b, c.u), c.k, c.v + gr.dx), dtype_is_float(S.dtype) ? Kind::Float : Kind::Int};
+      b -= back_shift;
+      return {tv(gr.idx, slot(depT(gr.idx), b, c.u), c.k, c.v + gr.dx), dtype_is_float(S.dtype) ? Kind::Float : Kind::Int};
     }
     // gather: per-element global load with clamped indices (any index form)
     const ReadSite& r = A.reads[ri];
@@ -354,11 +364,11 @@ struct Emitter {
         if (vb == va + V / 2) {
           if (gr.kind == RKind::STAGE && st_paired(gr.idx)) {
             const GStage& P = g.gs[gr.idx];
-            return R2{true, qname('n', gr.idx, slot(P.depth, P.hi - C.hi - gr.dy, u), k, va + gr.dx), {}, {}};
+            return R2{true, qname('n', gr.idx, slot(depS(gr.idx), P.hi - C.hi - gr.dy - back_shift, u), k, va + gr.dx), {}, {}};
           }
           if (gr.kind == RKind::STREAM && sr_paired(gr.idx)) {
             const GStream& S = g.streams[gr.idx];
-            return R2{true, qname('s', gr.idx, slot(S.depth, S.hi - C.hi - gr.dy, u), k, va + gr.dx), {}, {}};
+            return R2{true, qname('s', gr.idx, slot(depT(gr.idx), S.hi - C.hi - gr.dy - back_shift, u), k, va + gr.dx), {}, {}};
           }
         }
         R a = ex(e, Ctx{i, k, va, u}), b = ex(e, Ctx{i, k, vb, u});
@@ -405,6 +415,161 @@ struct Emitter {
     }
   }
 
+  // ---- incremental left-fold evaluation (interior kernel) ----
+  // A stage whose expression is a left-deep chain of float +,-,*,/ (the spine) over operands listed in
+  // row-major order can be evaluated row by row: the prefix that needs only older producer rows is computed
+  // as soon as those rows exist and carried forward as one value per element, instead of keeping the
+  // producer rows in a register window.  Same operations, same order => bit-identical (reading R3).
+  struct SpineOp { const Expr* node; const Expr* right; int pmb; };
+  struct Fold {
+    bool on = false;
+    const Expr* base = nullptr;
+    int base_pmb = 0;
+    std::vector<SpineOp> ops;
+    std::vector<int> m;            // distinct prefix min-backs, decreasing, last == 0
+    std::vector<int> cd;           // carried-value window depths m[j] - m[j+1]
+  };
+  std::vector<Fold> folds;
+  static constexpr int kInf = 1 << 28;
+
+  int minback(const Expr& e, int i) {
+    int mb = kInf;
+    if (e.op == Expr::ACCESS) {
+      const GRead& gr = g.greads.at(g.read_map.at(site.at(&e)));
+      if (gr.kind == RKind::STAGE) mb = g.gs[gr.idx].hi - g.gs[i].hi - gr.dy;
+      else if (gr.kind == RKind::STREAM) mb = g.streams[gr.idx].hi - g.gs[i].hi - gr.dy;
+    }
+    for (auto& a : e.args) mb = std::min(mb, minback(*a, i));
+    return mb;
+  }
+
+  // window depths needed by the reads of `e` evaluated `shift` steps ahead
+  void scan_depths(const Expr& e, int i, int shift, std::vector<int>& ds, std::vector<int>& dt) {
+    if (e.op == Expr::ACCESS) {
+      const GRead& gr = g.greads.at(g.read_map.at(site.at(&e)));
+      if (gr.kind == RKind::STAGE) ds[gr.idx] = std::max(ds[gr.idx], g.gs[gr.idx].hi - g.gs[i].hi - gr.dy - shift + 1);
+      else if (gr.kind == RKind::STREAM) dt[gr.idx] = std::max(dt[gr.idx], g.streams[gr.idx].hi - g.gs[i].hi - gr.dy - shift + 1);
+    }
+    for (auto& a : e.args) scan_depths(*a, i, shift, ds, dt);
+  }
+
+  static int gcd_(int a, int b) { return b ? gcd_(b, a % b) : a; }
+
+  // decide folds, fast window depths and the unroll factor of the interior kernel
+  void plan_interior() {
+    const int n = (int)g.gs.size();
+    folds.assign(n, Fold{});
+    const char* env = getenv("PMG_FOLD");
+    const bool enable = !(env && env[0] == '0') && !pair_on();
+    for (int i = 0; i < n && enable; ++i) {
+      const StageDecl& sd = p.stages[g.gs[i].id];
+      if (sd.dtype != DType::F32) continue;
+      Fold f;
+      const Expr* cur = sd.expr.get();
+      while (cur->op == Expr::BIN && cur->kind == Kind::Float &&
+             (cur->text == "+" || cur->text == "-" || cur->text == "*" ||
+              (cur->text == "/" && cur->args[1]->op == Expr::FLT))) {
+        f.ops.push_back({cur, cur->args[1].get(), 0});
+        cur = cur->args[0].get();
+      }
+      std::reverse(f.ops.begin(), f.ops.end());
+      f.base = cur;
+      int pm = minback(*cur, i);
+      std::vector<int> seq;
+      for (auto& op : f.ops) {
+        pm = std::min(pm, minback(*op.right, i));
+        op.pmb = pm;
+      }
+      // leading constant-only prefixes join the first segment that reads something
+      int first = kInf;
+      for (auto& op : f.ops)
+        if (op.pmb < kInf) { first = op.pmb; break; }
+      f.base_pmb = std::min(minback(*cur, i), first);
+      if (f.base_pmb >= kInf) continue;
+      for (auto& op : f.ops)
+        if (op.pmb >= kInf) op.pmb = f.base_pmb;
+      f.m.push_back(f.base_pmb);
+      for (auto& op : f.ops)
+        if (op.pmb != f.m.back()) f.m.push_back(op.pmb);
+      if (f.m.size() < 2 || f.m.back() != 0) continue;
+      for (size_t j = 0; j + 1 < f.m.size(); ++j) f.cd.push_back(f.m[j] - f.m[j + 1]);
+      f.on = true;
+      folds[i] = f;
+    }
+    auto compute = [&](std::vector<int>& ds, std::vector<int>& dt) {
+      ds.assign(n, 1);
+      dt.assign(g.streams.size(), 1);
+      for (int i = 0; i < n; ++i) {
+        const Fold& f = folds[i];
+        if (!f.on) { scan_depths(*p.stages[g.gs[i].id].expr, i, 0, ds, dt); continue; }
+        scan_depths(*f.base, i, f.base_pmb, ds, dt);
+        for (auto& op : f.ops) scan_depths(*op.right, i, op.pmb, ds, dt);
+      }
+    };
+    compute(dS, dT);
+    int U = 1;
+    auto lcm = [](int a, int b) { return a / gcd_(a, b) * b; };
+    for (int d : dS) U = lcm(U, d);
+    for (int d : dT) U = lcm(U, d);
+    for (auto& f : folds)
+      for (int d : f.cd) U = lcm(U, d);
+    if (U > 16) {   // give up folding: plain windows, shift mode beyond 16
+      folds.assign(n, Fold{});
+      dS.clear();
+      dT.clear();
+      Uk = g.U;
+      return;
+    }
+    Uk = U;
+  }
+
+  std::string cname(int i, int j, int sl, int k, int v) const {
+    return "f" + std::to_string(i) + "_" + std::to_string(j) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_e" + std::to_string(v);
+  }
+
+  // one spine operation with the running prefix as left operand (mirrors bin(): exact fma for 2^k*b)
+  R spine_op(const SpineOp& op, const R& left, const Ctx& c) {
+    const std::string& t = op.node->text;
+    if (t == "+" || t == "-") {
+      const Expr* mb;
+      float m;
+      if (pow2_mul(*op.right, &mb, &m))
+        return {"pmg_fma_exact(" + flit(t == "+" ? m : -m) + ", " + ex(*mb, c).s + ", " + tof(left).s + ")", Kind::Float};
+    }
+    if (t == "/") {
+      int k;
+      float v = op.right->fval;
+      if (is_pow2_float(v, &k) && std::isnormal(1.0f / v)) return {"pmg_mul(" + tof(left).s + ", " + flit(1.0f / v) + ")", Kind::Float};
+      return {"pmg_div(" + tof(left).s + ", " + flit(v) + ")", Kind::Float};
+    }
+    R b = tof(ex(*op.right, c));
+    const char* f = t == "+" ? "pmg_add" : t == "-" ? "pmg_sub" : "pmg_mul";
+    return {std::string(f) + "(" + tof(left).s + ", " + b.s + ")", Kind::Float};
+  }
+
+  // emit fold segment j of stage i at sub-step u: consume carried[j-1], produce carried[j] or the stage row
+  void fold_segment(int i, int j, int u, int cur, const std::string& ind) {
+    const Fold& f = folds[i];
+    const int nseg = (int)f.m.size();
+    const StageDecl& sd = p.stages[g.gs[i].id];
+    back_shift = f.m[j];
+    for (int kk = 0; kk < TX; ++kk)
+      for (int v = 0; v < V; ++v) {
+        Ctx c{i, kk, v, u};
+        R val;
+        if (j == 0) val = ex(*f.base, c);
+        else {
+          const int d = f.cd[j - 1];
+          val = {cname(i, j - 1, slot(d, d, u), kk, v), Kind::Float};
+        }
+        for (auto& op : f.ops)
+          if (op.pmb == f.m[j]) val = spine_op(op, val, c);
+        if (j == nseg - 1) o << ind << sv(i, cur, kk, v) << " = " << conv_store(val, sd.dtype) << ";\n";
+        else o << ind << cname(i, j, slot(f.cd[j], 0, u), kk, v) << " = " << tof(val).s << ";\n";
+      }
+    back_shift = 0;
+  }
+
   // ---- kernel text ----
   int himax = 0, xlm = 0, xrm = 0;
 
@@ -417,11 +582,10 @@ struct Emitter {
     return m == 1 ? 1 : V / 2;
   }
 
-  int phase_of(int t) const { return (((t - g.t_first) % g.U) + g.U) % g.U; }
+  int phase_of(int t) const { return (((t - g.t_first) % Uk) + Uk) % Uk; }
 
   std::string run() {
     const KConfig& k = g.cfg;
-    const int n = (int)g.gs.size();
     o << "// generated by libpmg (emit.cpp) for group " << g.name << ": ";
     for (auto& s : g.gs) o << p.stages[s.id].name << " ";
     o << "\n#include \"pmg_otpw.cuh\"\n\n";
@@ -437,9 +601,44 @@ struct Emitter {
     int nt = std::max<int>(1, (int)g.tensors.size()), ntab = std::max<int>(1, (int)p.tables.size()),
         np = std::max<int>(1, (int)p.params.size());
     o << "struct PmgArgs {\n  PmgTensor t[" << nt << "];\n  const char* tab[" << ntab << "];\n  int tabn[" << ntab
-      << "];\n  int prm[" << np << "];\n  int H, W, gy0, gy1, nty, ntx, npl, nfr, ntiles, pad_;\n};\n\n";
+      << "];\n  int prm[" << np << "];\n"
+         "  int H, W, gy0, gy1, nty, ntx, npl, nfr, ntiles, pad_;\n"
+         "  int txA, txB, tyA, tyB;   // interior rectangle of tile columns / rows (host-computed)\n};\n\n";
+    // tile index -> (tx, ty, pc, fr): interior kernel walks the rectangle, border kernel its complement
+    o << "__device__ __forceinline__ void pmg_tile_int(const PmgArgs& a, int t, int& tx, int& ty, int& pc, int& fr) {\n"
+         "  const int w = a.txB - a.txA, h = a.tyB - a.tyA;\n"
+         "  tx = a.txA + t % w; int r = t / w; ty = a.tyA + r % h; r /= h; pc = r % a.npl; fr = r / a.npl;\n}\n"
+         "__device__ __forceinline__ void pmg_tile_bdr(const PmgArgs& a, int t, int& tx, int& ty, int& pc, int& fr) {\n"
+         "  const int per = a.nty * a.ntx - (a.tyB - a.tyA) * (a.txB - a.txA);\n"
+         "  int kk = t % per; const int r = t / per; pc = r % a.npl; fr = r / a.npl;\n"
+         "  const int top = a.tyA * a.ntx;\n"
+         "  if (kk < top) { ty = kk / a.ntx; tx = kk % a.ntx; return; }\n"
+         "  kk -= top;\n"
+         "  const int bot = (a.nty - a.tyB) * a.ntx;\n"
+         "  if (kk < bot) { ty = a.tyB + kk / a.ntx; tx = kk % a.ntx; return; }\n"
+         "  kk -= bot;\n"
+         "  const int side = a.ntx - (a.txB - a.txA);\n"
+         "  ty = a.tyA + kk / side; const int j = kk % side; tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
+    kernel(true);
+    kernel(false);
+    return o.str();
+  }
+
+  // one entry point: interior tiles (branch-free bodies) or border tiles (general bodies)
+  void kernel(bool interior) {
+    const KConfig& k = g.cfg;
+    const int n = (int)g.gs.size();
+    if (interior) plan_interior();
+    else {
+      dS.clear();
+      dT.clear();
+      folds.assign(n, Fold{});
+      Uk = g.U;
+    }
+    const char* dec = interior ? "pmg_tile_int" : "pmg_tile_bdr";
     int minb = k.regcap > 0 ? std::max(1, 65536 / (k.regcap * 32 * k.NW)) : 1;
-    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << "(const __grid_constant__ PmgArgs a) {\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << (interior ? "" : "_b")
+      << "(const __grid_constant__ PmgArgs a) {\n";
     o << "  extern __shared__ __align__(128) char pmg_smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
          "  const int wib = threadIdx.x >> 5;\n"
@@ -467,7 +666,7 @@ struct Emitter {
       o << "  auto p_params = [&](int tile, int& y0r, u32& tot";
       for (size_t j = 0; j < g.streams.size(); ++j) o << ", const char*& src" << j << ", u32& dst" << j << ", u32& byt" << j;
       o << ") {\n"
-           "    const int txq = tile % a.ntx, rq = tile / a.ntx, tyq = rq % a.nty, rq2 = rq / a.nty, pcq = rq2 % a.npl, frq = rq2 / a.npl;\n"
+           "    int txq, tyq, pcq, frq;\n    " << dec << "(a, tile, txq, tyq, pcq, frq);\n"
            "    (void)pcq; (void)frq;\n"
            "    y0r = a.gy0 + tyq * TH;\n"
            "    const int cxq = txq * OW - PL;\n"
@@ -500,13 +699,12 @@ struct Emitter {
     }
     o << "  for (int it = 0; it < my_tiles; ++it) {\n"
          "    const int tile = gw + it * nwt;\n"
-         "    const int tx = tile % a.ntx, rr = tile / a.ntx, ty = rr % a.nty, rr2 = rr / a.nty, pc = rr2 % a.npl, fr = rr2 / a.npl;\n"
+         "    int tx, ty, pc, fr;\n    " << dec << "(a, tile, tx, ty, pc, fr);\n"
          "    const int y0 = a.gy0 + ty * TH;\n"
          "    const int cx = tx * OW - PL;\n"
          "    const int xL = cx + V * lane;\n"
          "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W);\n"
          "    const int yend = (y0 + TH < a.gy1) ? (y0 + TH) : a.gy1;\n"
-         "    const bool interior = !xb && (y0 + TFIRST >= 0) && (y0 + TH + HIMAX <= H) && (y0 + TH <= a.gy1);\n"
          "    (void)pc; (void)fr; (void)xL; (void)xb; (void)yend;\n";
     if (hs) {
       o << "    const bool has_next = it + 1 < my_tiles;\n"
@@ -524,59 +722,76 @@ struct Emitter {
     }
     for (int i = 0; i < n; ++i) {
       const GStage& P = g.gs[i];
-      declare('n', i, st_paired(i), p.stages[P.id].dtype == DType::F32, P.depth, P.el, P.er);
+      declare('n', i, st_paired(i), p.stages[P.id].dtype == DType::F32, depS(i), P.el, P.er);
     }
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
-      declare('s', (int)j, sr_paired((int)j), S.dtype == DType::F32, S.depth, S.el, S.er);
+      declare('s', (int)j, sr_paired((int)j), S.dtype == DType::F32, depT((int)j), S.el, S.er);
     }
-    // ---- interior tiles: branch-free bodies (warm-up unrolled, main loop, tail) ----
-    o << "    if (interior) {\n";
-    if (hs) {
-      for (size_t j = 0; j < g.streams.size(); ++j)
-        o << "      const char* q_ptr" << j << " = p_src" << j << " + (i64)(p_y0 + (TFIRST + " << g.streams[j].hi
-          << " + PREF)) * a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
+    for (int i = 0; i < n; ++i) {
+      const Fold& f = folds[i];
+      for (size_t j = 0; j < f.cd.size(); ++j) {
+        o << "    float ";
+        bool first = true;
+        for (int sl = 0; sl < f.cd[j]; ++sl)
+          for (int kk = 0; kk < TX; ++kk)
+            for (int v = 0; v < V; ++v) {
+              o << (first ? "" : ", ") << cname(i, (int)j, sl, kk, v) << " = 0.f";
+              first = false;
+            }
+        o << ";   // carried fold prefix of stage " << p.stages[g.gs[i].id].name << "\n";
+      }
     }
-    for (int t = g.t_first; t < 0; ++t) {
-      int s_ = t - g.t_first + k.PREF;
-      step(true, phase_of(t), true, t, s_ < g.nsteps ? 1 : 0);
-    }
-    // main section: the refill of every step targets this tile (pointer increment, no clamp)
-    const int a_end = std::max(0, k.TH - k.PREF) / g.U * g.U;
-    if (a_end > 0) {
-      o << "      for (int tb = 0; tb < " << a_end << "; tb += USTEP) {\n";
-      for (int u = 0; u < g.U; ++u) {
-        o << "      { const int t = tb + " << u << ";\n";
-        step(true, phase_of(u), false, 0, 1);
+    if (interior) {
+      // ---- interior tiles: branch-free bodies (warm-up unrolled, main loop, tail) ----
+      o << "    {\n";
+      if (hs) {
+        for (size_t j = 0; j < g.streams.size(); ++j)
+          o << "      const char* q_ptr" << j << " = p_src" << j << " + (i64)(p_y0 + (TFIRST + " << g.streams[j].hi
+            << " + PREF)) * a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
+      }
+      for (int t = g.t_first; t < 0; ++t) {
+        int s_ = t - g.t_first + k.PREF;
+        step(true, phase_of(t), true, t, s_ < g.nsteps ? 1 : 0);
+      }
+      // main section: the refill of every step targets this tile (pointer increment, no clamp)
+      const int a_end = std::max(0, k.TH - k.PREF) / Uk * Uk;
+      if (a_end > 0) {
+        o << "      for (int tb = 0; tb < " << a_end << "; tb += " << Uk << ") {\n";
+        for (int u = 0; u < Uk; ++u) {
+          o << "      { const int t = tb + " << u << ";\n";
+          step(true, phase_of(u), false, 0, 1);
+          o << "      }\n";
+        }
         o << "      }\n";
       }
-      o << "      }\n";
-    }
-    if (a_end < k.TH) {
-      // tail: the refills cross into the next tile (selects, clamped rows)
-      o << "      for (int tb = " << a_end << "; tb < TH; tb += USTEP) {\n";
-      for (int u = 0; u < g.U; ++u) {
+      if (a_end < k.TH) {
+        // tail: the refills cross into the next tile (selects, clamped rows)
+        o << "      for (int tb = " << a_end << "; tb < TH; tb += " << Uk << ") {\n";
+        for (int u = 0; u < Uk; ++u) {
+          o << "      { const int t = tb + " << u << ";\n      if (t < TH) {\n";
+          step(true, phase_of(u), false, 0, 0);
+          o << "      }\n      }\n";
+        }
+        o << "      }\n";
+      }
+      o << "    }\n";
+    } else {
+      // ---- border tiles: general bodies (clamped reads, edge replication, row checks) ----
+      o << "    for (int tb = TFIRST; tb < TH; tb += " << Uk << ") {\n";
+      for (int u = 0; u < Uk; ++u) {
         o << "      { const int t = tb + " << u << ";\n      if (t < TH) {\n";
-        step(true, phase_of(u), false, 0, 0);
+        step(false, u, false, 0, 0);
         o << "      }\n      }\n";
       }
-      o << "      }\n";
+      o << "    }\n";
     }
-    // ---- border tiles: general bodies (clamped reads, edge replication, row checks) ----
-    o << "    } else {\n      for (int tb = TFIRST; tb < TH; tb += USTEP) {\n";
-    for (int u = 0; u < g.U; ++u) {
-      o << "      { const int t = tb + " << u << ";\n      if (t < TH) {\n";
-      step(false, u, false, 0, 0);
-      o << "      }\n      }\n";
-    }
-    o << "      }\n    }\n";
     if (hs) {
       o << "    p_y0 = pn_y0; p_total = pn_total;\n";
       for (size_t j = 0; j < g.streams.size(); ++j)
         o << "    p_src" << j << " = pn_src" << j << "; p_dst" << j << " = pn_dst" << j << "; p_bytes" << j << " = pn_bytes" << j << ";\n";
     }
-    o << "  }\n}\n";
-    return o.str();
+    o << "  }\n}\n\n";
   }
 
   void shift_window(bool stage, int i, int depth, int el, int er, const std::string& ind) {
@@ -593,9 +808,10 @@ struct Emitter {
       << ind << "{\n" << ind << "const char* srow = ring + slq * RING;\n";
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
-      bool rot = S.depth <= 1 || g.U % S.depth == 0;
-      if (!rot) shift_window(false, (int)j, S.depth, S.el, S.er, ind);
-      int sl = rot ? slot(S.depth, 0, u) : 0;
+      const int SD = depT((int)j);
+      bool rot = SD <= 1 || Uk % SD == 0;
+      if (!rot) shift_window(false, (int)j, SD, S.el, S.er, ind);
+      int sl = rot ? slot(SD, 0, u) : 0;
       std::string ct = ctype(S.dtype);
       int lo = -S.el, hi = V + S.er;
       int vlo = (int)std::floor((double)lo / V) * V, vhi = (int)std::ceil((double)hi / V) * V;
@@ -724,12 +940,27 @@ struct Emitter {
     for (int i = 0; i < n; ++i) {
       const GStage& P = g.gs[i];
       const StageDecl& sd = p.stages[P.id];
-      if (tconst && tval < P.lo - P.hi) continue;   // not active yet (warm-up)
-      bool rot = P.depth <= 1 || g.U % P.depth == 0;
-      int cur = rot ? slot(P.depth, 0, u) : 0;
-      int prev = rot ? slot(P.depth, 1, u) : 1;
+      const bool folded = fast && folds.size() == g.gs.size() && folds[i].on;
+      const int T0 = P.lo - P.hi;
+      const int lead = folded ? folds[i].m[0] : 0;                  // earliest fold segment runs `lead` steps ahead
+      if (tconst && tval + lead < T0) continue;                      // not active yet (warm-up)
+      const bool fin = !tconst || tval >= T0;                       // the stage's own row this step
+      const int PD = depS(i);
+      bool rot = PD <= 1 || Uk % PD == 0;
+      int cur = rot ? slot(PD, 0, u) : 0;
+      int prev = rot ? slot(PD, 1, u) : 1;
       std::string rowv = "row" + std::to_string(i);
-      o << ind << "// stage " << sd.name << " (hi " << P.hi << ", lo " << P.lo << ", window " << P.depth << ")\n";
+      o << ind << "// stage " << sd.name << " (hi " << P.hi << ", lo " << P.lo << ", window " << PD << ")\n";
+      if (folded && !fin) {   // warm-up: only the early fold segments of later rows
+        for (int j = (int)folds[i].m.size() - 2; j >= 0; --j) {
+          if (tval + folds[i].m[j] < T0) continue;
+          o << ind << "{ // fold segment " << j << " (row +" << folds[i].m[j] << ")\n"
+            << ind << "const int " << rowv << " = y0 + t + (" << P.hi + folds[i].m[j] << ");\n" << ind << "(void)" << rowv << ";\n";
+          fold_segment(i, j, u, cur, ind + "  ");
+          o << ind << "}\n";
+        }
+        continue;
+      }
       std::string in2 = ind;
       if (!fast) {
         o << ind << "if (t >= " << (P.lo - P.hi) << ") {\n";
@@ -738,7 +969,7 @@ struct Emitter {
         o << ind << "{\n";
       }
       o << in2 << "const int " << rowv << " = y0 + t + (" << P.hi << ");\n" << in2 << "(void)" << rowv << ";\n";
-      if (!rot) shift_window(true, i, P.depth, P.el, P.er, in2);
+      if (!rot) shift_window(true, i, PD, P.el, P.er, in2);
       std::string in3 = in2;
       if (!fast) {
         o << in2 << "if (" << rowv << " >= 0 && " << rowv << " < H) {\n";
@@ -750,6 +981,8 @@ struct Emitter {
             R2 r = ex2(*sd.expr, i, kk, v, v + V / 2, u);
             o << in3 << qname('n', i, cur, kk, v) << " = " << pack(r) << ";\n";
           }
+      } else if (folded) {
+        fold_segment(i, (int)folds[i].m.size() - 1, u, cur, in3);   // consumes the carried prefix first
       } else {
         for (int kk = 0; kk < TX; ++kk)
           for (int v = 0; v < V; ++v) {
@@ -794,9 +1027,9 @@ struct Emitter {
       }
       if (st_paired(i)) complete_pairs('n', i, cur, P.el, P.er, in3);
       if (!fast) {
-        if (P.depth > 1) {
+        if (PD > 1) {
           o << in3 << "if (" << rowv << " == 0) {\n";
-          for (int sl = 0; sl < P.depth; ++sl)
+          for (int sl = 0; sl < PD; ++sl)
             if (sl != cur) copy_row('n', i, st_paired(i), P.el, P.er, cur, sl, in3 + "  ");
           o << in3 << "}\n" << in2 << "} else if (" << rowv << " >= H) {\n";
           copy_row('n', i, st_paired(i), P.el, P.er, prev, cur, in3);
@@ -804,6 +1037,14 @@ struct Emitter {
         o << in2 << "}\n";
       }
       if (P.materialize) store(i, cur, fast, tconst, tval, in2);
+      if (folded)   // earlier segments of later rows (after the final segment consumed their old values)
+        for (int j = (int)folds[i].m.size() - 2; j >= 0; --j) {
+          if (tconst && tval + folds[i].m[j] < T0) continue;
+          o << in2 << "{ // fold segment " << j << " (row +" << folds[i].m[j] << ")\n"
+            << in2 << "const int " << rowv << " = y0 + t + (" << P.hi + folds[i].m[j] << ");\n" << in2 << "(void)" << rowv << ";\n";
+          fold_segment(i, j, u, cur, in2 + "  ");
+          o << in2 << "}\n";
+        }
       o << ind << "}\n";
     }
     if (!g.streams.empty()) refill(tconst, tval, rmode, ind);

@@ -56,11 +56,24 @@ static const char* kOptions[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--
                                  "--ptxas-options=-v", "-default-device", "-DPMG_NVRTC=1"};
 
 static void parse_ptxas(Compiled& c) {
+  // per entry point: "Compiling entry function 'X'" ... "N bytes spill stores, M bytes spill loads" ... "Used R registers"
+  std::string cur;
+  std::istringstream in(c.log);
+  std::string line;
   std::smatch m;
-  if (std::regex_search(c.log, m, std::regex("Used ([0-9]+) registers"))) c.regs = std::stoi(m[1]);
-  if (std::regex_search(c.log, m, std::regex("([0-9]+) bytes spill stores, ([0-9]+) bytes spill loads"))) {
-    c.spill_stores = std::stoi(m[1]);
-    c.spill_loads = std::stoi(m[2]);
+  while (std::getline(in, line)) {
+    if (std::regex_search(line, m, std::regex("Compiling entry function '([A-Za-z0-9_]+)'"))) cur = m[1];
+    else if (std::regex_search(line, m, std::regex("([0-9]+) bytes spill stores, ([0-9]+) bytes spill loads"))) {
+      c.fns[cur].spill_stores = std::stoi(m[1]);
+      c.fns[cur].spill_loads = std::stoi(m[2]);
+    } else if (std::regex_search(line, m, std::regex("Used ([0-9]+) registers"))) c.fns[cur].regs = std::stoi(m[1]);
+  }
+  auto it = c.fns.find(c.name);
+  if (it == c.fns.end() && !c.fns.empty()) it = c.fns.begin();
+  if (it != c.fns.end()) {
+    c.regs = it->second.regs;
+    c.spill_stores = it->second.spill_stores;
+    c.spill_loads = it->second.spill_loads;
   }
   if (std::regex_search(c.log, m, std::regex("([0-9]+) bytes smem"))) c.smem_static = std::stoi(m[1]);
 }
@@ -221,18 +234,26 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     k.bin = jit_compile(g.name, g.source);
     check(D.ModuleLoadData(&k.mod, k.bin.cubin.data()), "cuModuleLoadData");
     check(D.ModuleGetFunction(&k.fn, k.mod, g.name.c_str()), "cuModuleGetFunction");
-    if (g.block_smem > 48 * 1024)
-      check(D.FuncSetAttribute(k.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, g.block_smem), "cuFuncSetAttribute");
+    check(D.ModuleGetFunction(&k.fn_b, k.mod, (g.name + "_b").c_str()), "cuModuleGetFunction");
+    for (CUfunction f : {k.fn, k.fn_b})
+      if (g.block_smem > 48 * 1024)
+        check(D.FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, g.block_smem), "cuFuncSetAttribute");
     check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm, k.fn, g.cfg.NW * 32, g.block_smem), "occupancy");
-    if (k.blocks_per_sm < 1) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
+    check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm_b, k.fn_b, g.cfg.NW * 32, g.block_smem), "occupancy");
+    if (k.blocks_per_sm < 1 || k.blocks_per_sm_b < 1) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
+    const FnStats& fb = k.bin.fns[g.name + "_b"];
     js << (gi ? "," : "") << "{\"name\":\"" << g.name << "\",\"regs\":" << k.bin.regs << ",\"spill_stores\":"
        << k.bin.spill_stores << ",\"spill_loads\":" << k.bin.spill_loads << ",\"block_smem\":" << g.block_smem
-       << ",\"blocks_per_sm\":" << k.blocks_per_sm << ",\"cached\":" << (k.bin.from_cache ? "true" : "false")
-       << ",\"compile_s\":" << k.bin.compile_s << "}";
+       << ",\"blocks_per_sm\":" << k.blocks_per_sm << ",\"border_regs\":" << fb.regs << ",\"border_spill_stores\":"
+       << fb.spill_stores << ",\"border_blocks_per_sm\":" << k.blocks_per_sm_b << ",\"cached\":"
+       << (k.bin.from_cache ? "true" : "false") << ",\"compile_s\":" << k.bin.compile_s << "}";
     P->kernels.push_back(std::move(k));
   }
   js << "],\"workspace_bytes\":" << P->ws_bytes << "}";
   P->json = js.str();
+  check(D.StreamCreate(&P->side, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  check(D.EventCreate(&P->ev_fork, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  check(D.EventCreate(&P->ev_join, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
   return P;
 }
 
@@ -242,6 +263,9 @@ void plan_destroy(Plan* P) {
     CtxGuard g(P->ctx);
     for (auto& k : P->kernels)
       if (k.mod) drv().ModuleUnload(k.mod);
+    if (P->side) drv().StreamDestroy(P->side);
+    if (P->ev_fork) drv().EventDestroy(P->ev_fork);
+    if (P->ev_join) drv().EventDestroy(P->ev_join);
     CUdevice dev;
     if (drv().DeviceGet(&dev, P->device) == CUDA_SUCCESS) drv().DevicePrimaryCtxRelease(dev);
   }
@@ -356,7 +380,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     const int NT = std::max<int>(1, (int)g.tensors.size()), NTAB = std::max(1, P.ntables),
               NP = std::max<int>(1, (int)p.params.size());
     size_t off_tab = 40 * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
-           off_int = off_prm + 4 * NP, size = (off_int + 40 + 7) / 8 * 8;
+           off_int = off_prm + 4 * NP, size = (off_int + 56 + 7) / 8 * 8;
     std::vector<char> buf(size, 0);
     for (size_t ti = 0; ti < g.tensors.size(); ++ti) {
       auto [is_stage, id] = g.tensors[ti];
@@ -414,13 +438,45 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     int64_t nty = (gy1 - gy0 + g.cfg.TH - 1) / g.cfg.TH;
     int64_t ntiles = (int64_t)nframes * g.npl * nty * g.ntx;
     if (ntiles > INT32_MAX) throw Error(-3, "too many tiles");
-    int32_t ints[10] = {Hg, Wg, gy0, gy1, (int32_t)nty, (int32_t)g.ntx, (int32_t)g.npl, (int32_t)nframes, (int32_t)ntiles, 0};
-    std::memcpy(buf.data() + off_int, ints, 40);
-    int64_t blocks_needed = (ntiles + g.cfg.NW - 1) / g.cfg.NW;
-    int64_t grid = std::min<int64_t>(blocks_needed, (int64_t)K.blocks_per_sm * P.spec.nsms);
+    // interior rectangle: tiles whose whole wavefront stays inside the image / the computed rows
+    // (matches the emitted bodies: no clamping, no x fix-up, no row checks needed there)
+    int xlm = 0, xrm = 0, himax = 0;
+    for (auto& st : g.streams) { xlm = std::max(xlm, st.xl); xrm = std::max(xrm, st.xr); himax = std::max(himax, st.hi); }
+    for (auto& st : g.gs) himax = std::max(himax, st.hi);
+    auto cdiv = [](int64_t a, int64_t b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
+    auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+    int64_t txA = std::max<int64_t>(0, cdiv(g.PL + xlm, g.OW));
+    int64_t txB = std::min<int64_t>(g.ntx, fdiv((int64_t)Wg - g.CW - xrm + g.PL, g.OW) + 1);
+    int64_t tyA = std::max<int64_t>(0, cdiv(-(int64_t)g.t_first - gy0, g.cfg.TH));
+    int64_t tyB = std::min<int64_t>({nty, fdiv((int64_t)Hg - g.cfg.TH - himax - gy0, g.cfg.TH) + 1,
+                                     fdiv((int64_t)gy1 - g.cfg.TH - gy0, g.cfg.TH) + 1});
+    if (txB <= txA || tyB <= tyA) txA = txB = tyA = tyB = 0;
+    const int64_t per = nty * g.ntx, n_int = (int64_t)nframes * g.npl * (tyB - tyA) * (txB - txA);
+    const int64_t n_bdr = (int64_t)nframes * g.npl * (per - (tyB - tyA) * (txB - txA));
     void* args[] = {buf.data()};
-    CUresult r = D.LaunchKernel(K.fn, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, s, args, nullptr);
-    if (r != CUDA_SUCCESS) throw Error(-6, "launch of " + g.name + ": " + cu_err(r));
+    auto launch = [&](CUfunction f, int bps, int64_t nt, CUstream st, const char* what) {
+      int32_t ints[14] = {Hg, Wg, gy0, gy1, (int32_t)nty, (int32_t)g.ntx, (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0,
+                          (int32_t)txA, (int32_t)txB, (int32_t)tyA, (int32_t)tyB};
+      std::memcpy(buf.data() + off_int, ints, 56);
+      int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
+      CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);
+      if (r != CUDA_SUCCESS) throw Error(-6, std::string("launch of ") + g.name + what + ": " + cu_err(r));
+    };
+    if (n_bdr > 0 && n_int > 0) {
+      // border tiles on the side stream, forked from and joined back into the caller's stream
+      check(D.EventRecord(P.ev_fork, s), "cuEventRecord");
+      check(D.StreamWaitEvent(P.side, P.ev_fork, 0), "cuStreamWaitEvent");
+      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, P.side, "_b");
+      launch(K.fn, K.blocks_per_sm, n_int, s, "");
+      check(D.EventRecord(P.ev_join, P.side), "cuEventRecord");
+      check(D.StreamWaitEvent(s, P.ev_join, 0), "cuStreamWaitEvent");
+    } else if (n_int > 0) {
+      launch(K.fn, K.blocks_per_sm, n_int, s, "");
+    } else if (n_bdr > 0) {
+      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, s, "_b");
+    }
+    (void)ntiles;
+
   }
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -10,10 +11,13 @@
 
 namespace pmg {
 
+struct FnStats { int regs = -1, spill_stores = -1, spill_loads = -1; };
+
 struct Compiled {
   std::string name, source, log;
   std::vector<char> cubin;
-  int regs = -1, spill_stores = -1, spill_loads = -1, smem_static = -1;
+  int regs = -1, spill_stores = -1, spill_loads = -1, smem_static = -1;   // the interior entry point
+  std::map<std::string, FnStats> fns;                                     // every entry point
   bool from_cache = false;
   double compile_s = 0;
 };
@@ -30,8 +34,8 @@ struct WsTensor {          // workspace placement of an intermediate (materialis
 struct Kernel {
   Compiled bin;
   CUmodule mod = nullptr;
-  CUfunction fn = nullptr;
-  int blocks_per_sm = 0;
+  CUfunction fn = nullptr, fn_b = nullptr;   // interior tiles / border tiles
+  int blocks_per_sm = 0, blocks_per_sm_b = 0;
 };
 
 struct Plan {
@@ -46,6 +50,8 @@ struct Plan {
   std::vector<WsTensor> ws;
   size_t ws_bytes = 0;
   int nimages = 0, ntables = 0, nout = 0;
+  CUstream side = nullptr;                 // border-tile kernels run here, forked/joined with events
+  CUevent ev_fork = nullptr, ev_join = nullptr;
   std::string json;
 };
 

@@ -41,7 +41,7 @@ def harris(img):
     for y in range(H):
         for x in range(W):
             g = lambda dy, dx: _get(img, y + dy, x + dx)  # noqa: E731
-            Iy[y, x] = ((((((g(1, -1) - g(-1, -1)) - two * g(-1, 0)) - g(-1, 1)) + two * g(1, 0))
+            Iy[y, x] = ((((((-g(-1, -1) - two * g(-1, 0)) - g(-1, 1)) + g(1, -1)) + two * g(1, 0))
                          + g(1, 1)) * k12)
             Ix[y, x] = ((((((g(-1, 1) - g(-1, -1)) - two * g(0, -1)) + two * g(0, 1)) - g(1, -1))
                          + g(1, 1)) * k12)
