@@ -337,18 +337,14 @@ struct Emitter {
   std::string pack(const R2& r) { return r.pair ? r.p : "make_float2(" + tof(r.a).s + ", " + tof(r.b).s + ")"; }
 
   bool pairable(const Expr& e) {
+    // packed pairs only for +, - (including the exact 2^k fma form), negation, literals and reads.
+    // Products and quotients stay scalar: ptxas fuses mul.rn.f32x2 -> add.rn.f32x2 into FFMA2 even with
+    // --fmad=false, which would change the rounding (checked on nvcc 12.9 / sm_100a).
     if (e.kind != Kind::Float) return false;
     switch (e.op) {
       case Expr::FLT: case Expr::ACCESS: return true;
       case Expr::UN: return e.text == "-";
-      case Expr::BIN:
-        if (e.text == "+" || e.text == "-" || e.text == "*") return true;
-        if (e.text == "/" && e.args[1]->op == Expr::FLT) {
-          int k;
-          return is_pow2_float(e.args[1]->fval, &k) && std::isnormal(1.0f / e.args[1]->fval);
-        }
-        return false;
-      case Expr::CALL: return e.text == "lerp";
+      case Expr::BIN: return e.text == "+" || e.text == "-";
       default: return false;
     }
   }
@@ -545,6 +541,51 @@ struct Emitter {
     R b = tof(ex(*op.right, c));
     const char* f = t == "+" ? "pmg_add" : t == "-" ? "pmg_sub" : "pmg_mul";
     return {std::string(f) + "(" + tof(left).s + ", " + b.s + ")", Kind::Float};
+  }
+
+  bool pack_on() const {
+    // opt-in (PMG_PACK=1): bit-exact, but on B200 the make_float2 MOVs cost what the packed FADD2s save
+    // (harris 6400^2: 0.1198 ms packed vs 0.1169 ms scalar)
+    const char* e = getenv("PMG_PACK");
+    return V >= 2 && V % 2 == 0 && e && e[0] == '1' && !pair_on();
+  }
+
+  // packed fold segment: statement per spine op; pairs (v, v + V/2) of the same lane
+  void fold_segment_pair(int i, int j, int u, int cur, const std::string& ind) {
+    const Fold& f = folds[i];
+    const int nseg = (int)f.m.size(), h = V / 2;
+    back_shift = f.m[j];
+    for (int kk = 0; kk < TX; ++kk)
+      for (int v = 0; v < h; ++v) {
+        Ctx ca{i, kk, v, u}, cb{i, kk, v + h, u};
+        o << ind << "{ float2 pv = ";
+        if (j == 0) o << pack(ex2(*f.base, i, kk, v, v + h, u));
+        else {
+          const int d = f.cd[j - 1];
+          o << "make_float2(" << cname(i, j - 1, slot(d, d, u), kk, v) << ", " << cname(i, j - 1, slot(d, d, u), kk, v + h) << ")";
+        }
+        o << ";\n";
+        for (auto& op : f.ops) {
+          if (op.pmb != f.m[j]) continue;
+          const std::string& t = op.node->text;
+          const Expr* mb;
+          float m;
+          if ((t == "+" || t == "-") && pow2_mul(*op.right, &mb, &m)) {
+            o << ind << "  pv = pmg_fma2(pmg_bc2(" << flit(t == "+" ? m : -m) << "), " << pack(ex2(*mb, i, kk, v, v + h, u)) << ", pv);\n";
+          } else if (t == "+" || t == "-") {
+            o << ind << "  pv = " << (t == "+" ? "pmg_add2" : "pmg_sub2") << "(pv, " << pack(ex2(*op.right, i, kk, v, v + h, u)) << ");\n";
+          } else {   // * and / element by element (scalar; see pairable())
+            R lx = spine_op(op, R{"pv.x", Kind::Float}, ca), ly = spine_op(op, R{"pv.y", Kind::Float}, cb);
+            o << ind << "  pv = make_float2(" << lx.s << ", " << ly.s << ");\n";
+          }
+        }
+        if (j == nseg - 1)
+          o << ind << "  " << sv(i, cur, kk, v) << " = pv.x; " << sv(i, cur, kk, v + h) << " = pv.y; }\n";
+        else
+          o << ind << "  " << cname(i, j, slot(f.cd[j], 0, u), kk, v) << " = pv.x; " << cname(i, j, slot(f.cd[j], 0, u), kk, v + h)
+            << " = pv.y; }\n";
+      }
+    back_shift = 0;
   }
 
   // emit fold segment j of stage i at sub-step u: consume carried[j-1], produce carried[j] or the stage row
@@ -956,7 +997,8 @@ struct Emitter {
           if (tval + folds[i].m[j] < T0) continue;
           o << ind << "{ // fold segment " << j << " (row +" << folds[i].m[j] << ")\n"
             << ind << "const int " << rowv << " = y0 + t + (" << P.hi + folds[i].m[j] << ");\n" << ind << "(void)" << rowv << ";\n";
-          fold_segment(i, j, u, cur, ind + "  ");
+          if (pack_on()) fold_segment_pair(i, j, u, cur, ind + "  ");
+          else fold_segment(i, j, u, cur, ind + "  ");
           o << ind << "}\n";
         }
         continue;
@@ -982,7 +1024,14 @@ struct Emitter {
             o << in3 << qname('n', i, cur, kk, v) << " = " << pack(r) << ";\n";
           }
       } else if (folded) {
-        fold_segment(i, (int)folds[i].m.size() - 1, u, cur, in3);   // consumes the carried prefix first
+        // consumes the carried prefix first
+        if (pack_on()) fold_segment_pair(i, (int)folds[i].m.size() - 1, u, cur, in3);
+        else fold_segment(i, (int)folds[i].m.size() - 1, u, cur, in3);
+      } else if (fast && pack_on() && sd.dtype == DType::F32 && pairable(*sd.expr)) {
+        for (int kk = 0; kk < TX; ++kk)
+          for (int v = 0; v < V / 2; ++v)
+            o << in3 << "{ const float2 pv = " << pack(ex2(*sd.expr, i, kk, v, v + V / 2, u)) << "; " << sv(i, cur, kk, v)
+              << " = pv.x; " << sv(i, cur, kk, v + V / 2) << " = pv.y; }\n";
       } else {
         for (int kk = 0; kk < TX; ++kk)
           for (int v = 0; v < V; ++v) {
@@ -1042,7 +1091,8 @@ struct Emitter {
           if (tconst && tval + folds[i].m[j] < T0) continue;
           o << in2 << "{ // fold segment " << j << " (row +" << folds[i].m[j] << ")\n"
             << in2 << "const int " << rowv << " = y0 + t + (" << P.hi + folds[i].m[j] << ");\n" << in2 << "(void)" << rowv << ";\n";
-          fold_segment(i, j, u, cur, in2 + "  ");
+          if (pack_on()) fold_segment_pair(i, j, u, cur, in2 + "  ");
+          else fold_segment(i, j, u, cur, in2 + "  ");
           o << in2 << "}\n";
         }
       o << ind << "}\n";
