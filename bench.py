@@ -204,6 +204,7 @@ def main():
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
+    launches_per_step = plan.last_launches
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{dev}")
@@ -289,7 +290,7 @@ def main():
                              "peak_derivation": f"128 FP32/INT32 lanes x {nsms} SMs x sm_max_mhz"},
                      "note": "bound = the larger of the HBM and ALU ideal times (DESIGN.md §6); "
                              f"{nk} kernel(s) per step, timed per step on the launching stream"},
-        "gpu_launches": nk * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "e2e": e2e,
     }

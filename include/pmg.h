@@ -28,7 +28,9 @@
  * PMG_ERR_INFEASIBLE: every candidate schedule has infinite cost (Alg. 2, 945, 961).
  *
  * Concurrency: a pipeline is immutable and shareable across threads; a plan may run concurrently on
- * different streams only with distinct workspaces.  Outputs are bit-identical for any schedule, band
+ * different streams only with distinct workspaces.  A run's launches are ordered on the caller's stream
+ * (border-tile kernels fork onto the plan's side stream and join back with events), so runs can be
+ * captured into CUDA graphs.  Outputs are bit-identical for any schedule, band
  * split or batch split (DESIGN.md §"Determinism").  No NCCL here: process groups and gathers belong to
  * the caller (PyTorch).
  */
@@ -167,7 +169,10 @@ pmg_status pmg_plan_create(pmg_pipeline p, const int64_t* params, int nparams, i
 void pmg_plan_destroy(pmg_plan plan); /* NULL-safe; caller ensures no run is in flight */
 pmg_status pmg_plan_describe(pmg_plan plan, char* buf, size_t cap, size_t* needed); /* JSON */
 pmg_status pmg_plan_workspace_bytes(pmg_plan plan, size_t* out);
-int pmg_plan_num_kernels(pmg_plan plan);
+int pmg_plan_num_kernels(pmg_plan plan);   /* fused groups (each launches an interior and/or a border kernel) */
+/* kernels the most recent run / run_batch / run_band call launched (0..2 per group: interior tiles on the
+ * caller's stream, border tiles on a forked side stream; empty classes are not launched); -1 for NULL */
+int pmg_plan_last_launches(pmg_plan plan);
 
 /* full-image run: in[] = images then tables (declaration order), out[] = liveouts */
 pmg_status pmg_run(pmg_plan plan, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace,

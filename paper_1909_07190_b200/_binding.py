@@ -96,6 +96,7 @@ _sig = {
     "pmg_plan_describe": (C.c_int, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "pmg_plan_workspace_bytes": (C.c_int, [P, C.POINTER(C.c_size_t)]),
     "pmg_plan_num_kernels": (C.c_int, [P]),
+    "pmg_plan_last_launches": (C.c_int, [P]),
     "pmg_run": (C.c_int, [P, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.c_void_p, C.c_void_p]),
     "pmg_run_batch": (C.c_int, [P, C.c_int, C.POINTER(Buf), I64P, C.c_int, C.POINTER(Buf), I64P, C.c_int,
                                 C.c_void_p, C.c_void_p]),

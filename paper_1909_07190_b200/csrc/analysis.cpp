@@ -10,6 +10,12 @@
 
 namespace pmg {
 
+static int64_t fdiv(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+
 namespace {
 
 // affine form over the consumer's normalised vars: sum coef[d]*v_d + c
@@ -193,16 +199,77 @@ std::array<int, 3> warp_sizes(const std::array<int, 3>& B, int ws) {
   return W;
 }
 
-static int64_t fdiv(int64_t a, int64_t b) {
-  int64_t q = a / b;
-  if ((a % b) && ((a < 0) != (b < 0))) --q;
-  return q;
+// interval of an integer index expression over a box of consumer coordinates (conservative; false = unknown).
+// Used for "general" row indices such as the pyramid upsample y/2 - 1 + 2*(y%2).
+static bool int_interval(const Expr& e, const int64_t lo[3], const int64_t hi[3], int cons_nd,
+                         const std::vector<int64_t>& params, int64_t& a, int64_t& b) {
+  if (e.kind != Kind::Int) return false;
+  int64_t a0, b0, a1, b1, a2, b2;
+  auto sub = [&](int i, int64_t& x, int64_t& y) { return int_interval(*e.args[i], lo, hi, cons_nd, params, x, y); };
+  switch (e.op) {
+    case Expr::INT: a = b = e.ival; return true;
+    case Expr::PARAM: a = b = params.at(e.index); return true;
+    case Expr::VAR: { int d = e.index + (3 - cons_nd); a = lo[d]; b = hi[d]; return true; }
+    case Expr::UN:
+      if (e.text != "-" || !sub(0, a0, b0)) return false;
+      a = -b0; b = -a0;
+      return true;
+    case Expr::BIN: {
+      if (!sub(0, a0, b0) || !sub(1, a1, b1)) return false;
+      const std::string& t = e.text;
+      if (t == "+") { a = a0 + a1; b = b0 + b1; return true; }
+      if (t == "-") { a = a0 - b1; b = b0 - a1; return true; }
+      if (t == "*") {
+        int64_t c[4] = {a0 * a1, a0 * b1, b0 * a1, b0 * b1};
+        a = *std::min_element(c, c + 4); b = *std::max_element(c, c + 4);
+        return true;
+      }
+      if (t == "/" && a1 == b1 && a1 > 0) { a = fdiv(a0, a1); b = fdiv(b0, a1); return true; }   // floor division
+      if (t == "%" && a1 == b1 && a1 > 0) {                                                       // non-negative
+        const int64_t m = a1, ra = a0 - fdiv(a0, m) * m, rb = b0 - fdiv(b0, m) * m;
+        if (b0 - a0 + 1 < m && ra <= rb) { a = ra; b = rb; } else { a = 0; b = m - 1; }
+        return true;
+      }
+      return false;
+    }
+    case Expr::CALL: {
+      const std::string& f = e.text;
+      if ((f == "min" || f == "max") && sub(0, a0, b0) && sub(1, a1, b1)) {
+        if (f == "min") { a = std::min(a0, a1); b = std::min(b0, b1); } else { a = std::max(a0, a1); b = std::max(b0, b1); }
+        return true;
+      }
+      if (f == "clamp" && sub(0, a0, b0) && sub(1, a1, b1) && sub(2, a2, b2)) {   // min(max(x, l), h)
+        a = std::min(std::max(a0, a1), a2);
+        b = std::min(std::max(b0, b1), b2);
+        return true;
+      }
+      if (f == "select" && sub(1, a1, b1) && sub(2, a2, b2)) { a = std::min(a1, a2); b = std::max(b1, b2); return true; }
+      if (f == "i32" && sub(0, a0, b0)) { a = a0; b = b0; return true; }
+      return false;
+    }
+    default: return false;
+  }
 }
 
 RowIv rows_needed(const Analysis& A, const ReadSite& r, RowIv cr, int64_t src_rows) {
-  (void)A;
   RowIv out{0, src_rows};
   if (cr.hi <= cr.lo) return RowIv{0, 0};
+  if (r.form[1] == Form::GENERAL) {
+    // interval analysis of the row index over the consumer's rows (other dims: their whole extent)
+    const Ext3& ce = A.stage_ext[r.consumer];
+    const int cnd = (int)A.p->stages[r.consumer].vars.size(), pnd = (int)r.node->args.size();
+    int64_t lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) { lo[d] = 0; hi[d] = ce.e[d] - 1; }
+    lo[1] = cr.lo;
+    hi[1] = cr.hi - 1;
+    int64_t a, b;
+    if (pnd >= 2 && int_interval(*r.node->args[pnd - 2], lo, hi, cnd, A.params, a, b)) {
+      out.lo = std::max<int64_t>(0, std::min(a, src_rows - 1));
+      out.hi = std::min<int64_t>(src_rows, std::max(b + 1, out.lo + 1));
+      return out;
+    }
+    return RowIv{0, src_rows};
+  }
   switch (r.form[1]) {
     case Form::UNIT: out = {cr.lo + r.off[1], cr.hi - 1 + r.off[1] + 1}; break;
     case Form::DOWN2: out = {2 * cr.lo + r.off[1], 2 * (cr.hi - 1) + r.off[1] + 1}; break;

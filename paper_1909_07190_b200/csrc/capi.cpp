@@ -326,6 +326,8 @@ pmg_status pmg_plan_workspace_bytes(pmg_plan plan, size_t* out) {
 
 int pmg_plan_num_kernels(pmg_plan plan) { return plan ? (int)plan->plan->kernels.size() : -1; }
 
+int pmg_plan_last_launches(pmg_plan plan) { return plan ? plan->plan->last_launches : -1; }
+
 pmg_status pmg_run(pmg_plan plan, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace, void* stream) {
   if (!plan || (!in && nin) || (!out && nout)) return fail(PMG_ERR_ARG, "NULL argument");
   PMG_TRY({

@@ -350,6 +350,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
   CUdevice cd;
   if (!cur || D.CtxGetDevice(&cd) != CUDA_SUCCESS || (int)cd != P.device)
     throw Error(-9, "the plan's device must be current on the calling thread");
+  P.last_launches = 0;
   if (P.ws_bytes && !ws) throw Error(-9, "workspace required");
   auto aligned = [](const pmg_buf& b) {
     return ((uintptr_t)b.ptr % 16 == 0) && (b.row_pitch_bytes % 16 == 0) && (b.plane_pitch_bytes % 16 == 0);
@@ -461,6 +462,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
       CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);
       if (r != CUDA_SUCCESS) throw Error(-6, std::string("launch of ") + g.name + what + ": " + cu_err(r));
+      ++P.last_launches;
     };
     if (n_bdr > 0 && n_int > 0) {
       // border tiles on the side stream, forked from and joined back into the caller's stream

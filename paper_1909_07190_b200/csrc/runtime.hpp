@@ -53,6 +53,7 @@ struct Plan {
   CUstream side = nullptr;                 // border-tile kernels run here, forked/joined with events
   CUevent ev_fork = nullptr, ev_join = nullptr;
   std::string json;
+  int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
 };
 
 std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,

@@ -209,6 +209,11 @@ class Plan:
     def num_kernels(self) -> int:
         return B.lib.pmg_plan_num_kernels(self._h)
 
+    @property
+    def last_launches(self) -> int:
+        """kernels launched by the most recent run call (interior + border kernels of every group)"""
+        return B.lib.pmg_plan_last_launches(self._h)
+
     def workspace(self, frames: int = 1):
         import torch
         need = max(16, self.workspace_bytes * frames)

@@ -204,6 +204,46 @@ def test_band_geometry_host():
     assert [b[2:] for b in bands] == [(0, 122), (118, 242), (238, 362), (358, 480)]   # +-2 rows of halo
 
 
+@pytest.mark.parametrize("wl,n", [
+    (PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 64, "H": 192}, 1005), 4),   # up/down + general y/2-1+2*(y%2)
+    (PI.small("camera", 64, 96), 3),
+    (PI.small("unsharp", 48, 64), 4),
+])
+def test_band_input_rows_suffice(wl, n):
+    """Band geometry pinned against the oracle, not against itself: replacing every input row
+    outside [in_r0, in_r1) by unrelated values must leave the band's output rows [out_r0, out_r1) unchanged.
+    For the local Laplacian this exercises the interval analysis of the non-affine upsample row index."""
+    import numpy as np
+    from oracle import evaluate
+    p = pmg.Pipeline(wl.text)
+    inp = wl.inputs()
+    full = evaluate(wl.text, wl.params, inp)
+    (key, ref), = full.items()
+    H = wl.params["H"]
+    rng = np.random.default_rng(7)
+    covered = []
+    for b in range(n):
+        o_r0, o_r1, i_r0, i_r1 = p.band_rows(wl.params, b, n, opts=pmg.sched_opts(probe=False))
+        covered.append((o_r0, o_r1))
+        pois = {}
+        for name, v in inp.items():
+            if v.ndim < 2:
+                pois[name] = v
+                continue
+            w = v.copy()
+            junk = (rng.integers(0, 1024, size=v.shape).astype(v.dtype) if v.dtype.kind in "iu"
+                    else rng.random(v.shape).astype(v.dtype))
+            w[..., :i_r0, :] = junk[..., :i_r0, :]
+            w[..., i_r1:, :] = junk[..., i_r1:, :]
+            pois[name] = w
+        got = evaluate(wl.text, wl.params, pois)[key]
+        np.testing.assert_array_equal(got[..., o_r0:o_r1, :].view(np.uint8), ref[..., o_r0:o_r1, :].view(np.uint8))
+        if 0 < b < n - 1:
+            assert i_r1 - i_r0 < H        # a middle band does not need the whole image
+    assert covered[0][0] == 0 and covered[-1][1] == H
+    assert all(covered[i][1] == covered[i + 1][0] for i in range(n - 1))
+
+
 # ------------------------------------------------------------------ emitted kernels: OTPW synchronisation
 @pytest.mark.parametrize("name", ["blur", "harris", "unsharp", "camera"])
 def test_emitted_kernels_use_only_warp_synchronisation(name):

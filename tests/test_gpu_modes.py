@@ -17,10 +17,11 @@ import paper_1909_07190_b200 as pmg  # noqa: E402
 
 @pytest.mark.parametrize("name,W,H,n,fuse", [("harris", 300, 211, 4, True), ("unsharp", 160, 97, 3, True),
                                              ("blur", 128, 128, 8, True), ("harris", 120, 90, 3, False),
-                                             ("camera", 132, 98, 2, True)])
+                                             ("camera", 132, 98, 2, True), ("ll", 96, 192, 4, True)])
 def test_band_invariance(name, W, H, n, fuse):
     import torch
-    wl = PI.small(name, W, H)
+    wl = (PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": W, "H": H}, 1005) if name == "ll"
+          else PI.small(name, W, H))
     inp = wl.inputs()
     full, plan = run_gpu(wl.text, wl.params, inp, opts=pmg.sched_opts(fuse=fuse))
     (key, ref), = full.items()
