@@ -661,6 +661,15 @@ struct Emitter {
          "  const int side = a.ntx - (a.txB - a.txA);\n"
          "  ty = a.tyA + kk / side; const int j = kk % side; tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
     kernel(true);
+    return o.str();
+  }
+
+  // the border-tile kernel of the same group, with TH_b-row tiles (macros TH / NSTEPS redefined)
+  std::string run_border() {
+    for (auto& P : g.gs) himax = std::max(himax, P.hi);
+    for (auto& S : g.streams) himax = std::max(himax, S.hi);
+    for (auto& S : g.streams) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
+    o << "#undef TH\n#undef NSTEPS\n#define TH " << g.cfg.TH << "\n#define NSTEPS " << g.nsteps << "\n\n";
     kernel(false);
     return o.str();
   }
@@ -1106,7 +1115,14 @@ struct Emitter {
 
 std::string emit_group(const Analysis& A, const Group& g) {
   Emitter e(A, g);
-  return e.run();
+  std::string src = e.run();
+  Group gb = g;                        // border kernel: same geometry with TH_b-row tiles
+  if (g.TH_b > 0) {
+    gb.cfg.TH = g.TH_b;
+    gb.nsteps = g.TH_b - g.t_first;
+  }
+  Emitter eb(A, gb);
+  return src + eb.run_border();
 }
 
 }  // namespace pmg

@@ -9,6 +9,7 @@
 //     already-computed row ("no cyclic dependence between two adjacent tiles");
 //   * warp sizes W = (32,1,1) from B = (32*NW,1,1); one overlapped tile per warp.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <set>
 
@@ -203,6 +204,15 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   for (auto& st : g.streams) g.t_first = std::min(g.t_first, st.lo - st.hi);
   g.nsteps = k.TH - g.t_first;
   if (!g.streams.empty() && k.PREF > g.nsteps) return bad("prefetch depth exceeds the steps of one tile");
+  // border tiles: one warp walks a whole tile through the general (clamping) body at low occupancy, so the
+  // border kernel's time is one tile's latency; it runs with shorter tiles (measured)
+  {
+    const char* e = getenv("PMG_BORDER_TH");
+    int want = e ? atoi(e) : 8;
+    g.TH_b = k.TH;
+    for (int d = std::min(want, k.TH); d >= 1; --d)
+      if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_b = d; break; }
+  }
   // unroll factor for register-window rotation
   int U = 1;
   auto lcm = [](int a, int b) { return a / std::gcd(a, b) * b; };

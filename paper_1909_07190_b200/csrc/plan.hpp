@@ -77,6 +77,7 @@ struct Group {
   std::vector<std::pair<bool, int>> tensors;  // slot -> (is_stage, id)
   int CW = 0, PL = 0, PR = 0, OW = 0;
   int t_first = 0, nsteps = 0, U = 1;
+  int TH_b = 0;             // tile rows of the border-tile kernel (divides TH; small: border tiles are latency-bound)
   int ring_bytes = 0;       // one ring slot
   int warp_smem = 0;        // bytes of shared memory per warp
   int block_smem = 0;

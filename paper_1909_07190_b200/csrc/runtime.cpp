@@ -453,11 +453,16 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
                                      fdiv((int64_t)gy1 - g.cfg.TH - gy0, g.cfg.TH) + 1});
     if (txB <= txA || tyB <= tyA) txA = txB = tyA = tyB = 0;
     const int64_t per = nty * g.ntx, n_int = (int64_t)nframes * g.npl * (tyB - tyA) * (txB - txA);
-    const int64_t n_bdr = (int64_t)nframes * g.npl * (per - (tyB - tyA) * (txB - txA));
+    (void)per;
+    // border kernel: the same regions in TH_b-row tiles (TH_b divides TH)
+    const int THb = g.TH_b > 0 ? g.TH_b : g.cfg.TH, rb = g.cfg.TH / THb;
+    const int64_t nty_b = (gy1 - gy0 + THb - 1) / THb, tyA_b = tyA * rb, tyB_b = tyB * rb;
+    const int64_t n_bdr = (int64_t)nframes * g.npl * (nty_b * g.ntx - (tyB_b - tyA_b) * (txB - txA));
     void* args[] = {buf.data()};
     auto launch = [&](CUfunction f, int bps, int64_t nt, CUstream st, const char* what) {
-      int32_t ints[14] = {Hg, Wg, gy0, gy1, (int32_t)nty, (int32_t)g.ntx, (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0,
-                          (int32_t)txA, (int32_t)txB, (int32_t)tyA, (int32_t)tyB};
+      const bool bd = f == K.fn_b;
+      int32_t ints[14] = {Hg, Wg, gy0, gy1, (int32_t)(bd ? nty_b : nty), (int32_t)g.ntx, (int32_t)g.npl, (int32_t)nframes,
+                          (int32_t)nt, 0, (int32_t)txA, (int32_t)txB, (int32_t)(bd ? tyA_b : tyA), (int32_t)(bd ? tyB_b : tyB)};
       std::memcpy(buf.data() + off_int, ints, 56);
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
       CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);

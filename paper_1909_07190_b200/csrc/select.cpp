@@ -95,6 +95,14 @@ static double ops_of(const Expr& e) {
 
 double stage_ops(const Pipeline& p, int s) { return std::max(1.0, ops_of(*p.stages[s].expr)); }
 
+// Alg. 2: the weighted sum of the seven terms
+static void weigh(CostBreakdown& c, const pmg_weights& w) {
+  double ratio = c.compute_time > 0 ? c.mem_time / c.compute_time : 0;
+  c.cost = w.w[0] * c.txs_per_point + w.w[1] * (1 - c.occupancy) + w.w[2] * ratio + w.w[3] * c.unallocated_sh_mem +
+           w.w[4] * c.unused_reg + w.w[5] * c.frac_overlap + w.w[6] * c.extra_tbs;                            // l.981
+  if (c.infinite) c.cost = std::numeric_limits<double>::infinity();
+}
+
 // ---- the shared tail of Alg. 2 (lines 957-982) ----
 static void alg2_tail(CostBreakdown& c, const pmg_gpu_spec& S, const pmg_weights& w, double tile_vol,
                       double time_per_iter_sum, double overlap_pts, double computed_pts, int tx_size) {
@@ -115,10 +123,7 @@ static void alg2_tail(CostBreakdown& c, const pmg_gpu_spec& S, const pmg_weights
   c.unused_reg = std::max(0.0, std::min(1.0, 1.0 - reg_per_sm * c.occupancy / S.regs_per_sm));               // l.978
   c.frac_overlap = computed_pts > 0 ? overlap_pts / computed_pts : 0.0;                                       // l.979 (R12)
   c.extra_tbs = c.max_tb_per_sm > 0 ? std::fmod(std::ceil(c.tb_per_sm), c.max_tb_per_sm) : 0;                // l.980 (R14)
-  double ratio = c.compute_time > 0 ? c.mem_time / c.compute_time : 0;
-  c.cost = w.w[0] * c.txs_per_point + w.w[1] * (1 - c.occupancy) + w.w[2] * ratio + w.w[3] * c.unallocated_sh_mem +
-           w.w[4] * c.unused_reg + w.w[5] * c.frac_overlap + w.w[6] * c.extra_tbs;                            // l.981
-  if (c.infinite) c.cost = std::numeric_limits<double>::infinity();
+  weigh(c, w);
 }
 
 // transactions of one warp access of `n` consecutive elements of `esz` bytes starting at byte `start` (MinGLTxs)
@@ -160,6 +165,18 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
     useful += out_pts;
   }
   alg2_tail(c, S, w, (double)g.CW * k.TH, tpi, computed - useful, computed, k.tx_size);
+  // B200 readings of two terms for the persistent OTPW grid (R21):
+  //  occupancy = resident warps per SM the launch can actually fill (a grid with fewer tiles than resident
+  //              slots leaves them empty), over MaxWarpsPerSM;
+  //  extraTBs  = idle fraction of the last wave of tiles, 1 - waves / ceil(waves) (0 below one wave, where the
+  //              shortfall is already in the occupancy term).
+  const double slots = c.occupancy * S.max_warps_per_sm, tiles_ = c.total_threads / S.warp_size;
+  if (slots > 0) {
+    c.occupancy = std::min(slots, tiles_ / S.nsms) / S.max_warps_per_sm;
+    const double waves = tiles_ / (slots * S.nsms);
+    c.extra_tbs = waves <= 1 ? 0.0 : 1.0 - waves / std::ceil(waves);
+  }
+  weigh(c, w);
   return c;
 }
 
