@@ -611,6 +611,18 @@ struct Emitter {
     back_shift = 0;
   }
 
+  int state_regs() {
+    plan_interior();
+    const int n = (int)g.gs.size();
+    int r = 0;
+    for (int i = 0; i < n; ++i) r += (depS(i) - 1) * TX * (V + g.gs[i].el + g.gs[i].er);
+    for (size_t j = 0; j < g.streams.size(); ++j)
+      r += (depT((int)j) - 1) * TX * (V + g.streams[j].el + g.streams[j].er);
+    for (auto& f : folds)
+      for (int d : f.cd) r += d * TX * V;
+    return r;
+  }
+
   // ---- kernel text ----
   int himax = 0, xlm = 0, xrm = 0;
 
@@ -1112,6 +1124,13 @@ struct Emitter {
 };
 
 }  // namespace
+
+// registers live across steps in the interior kernel (fold-aware windows, carried prefixes, input windows):
+// the selector's register estimate is fitted on this count (select.cpp)
+int interior_state_regs(const Analysis& A, const Group& g) {
+  Emitter e(A, g);
+  return e.state_regs();
+}
 
 std::string emit_group(const Analysis& A, const Group& g) {
   Emitter e(A, g);

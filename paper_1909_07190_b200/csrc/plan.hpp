@@ -90,6 +90,9 @@ struct Group {
 // build geometry; returns false (with g.why_infeasible) when the group cannot run as one kernel
 bool build_group(const Analysis& A, Group& g, const std::vector<int>& group_of_stage);
 
+// registers the interior kernel keeps live from one row step to the next (register-estimate input)
+int interior_state_regs(const Analysis& A, const Group& g);
+
 // CUDA C++ source of one group kernel (NVRTC input)
 std::string emit_group(const Analysis& A, const Group& g);
 

@@ -141,7 +141,6 @@ Compiled jit_compile(const std::string& name, const std::string& source) {
 
 RegProbe make_probe(const Analysis& A) {
   return [&A](const Group& g, int* regs, int* spill) {
-    if (g.regs_est <= 96) return false;   // far from the register limit: the estimate is enough
     Group h = g;
     h.name = "pmg_probe";
     Compiled c = jit_compile(h.name, emit_group(A, h));

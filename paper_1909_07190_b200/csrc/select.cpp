@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -133,7 +135,89 @@ static double min_txs(int64_t start, int64_t nbytes, int tx) {
   return double(b - a + 1);
 }
 
-CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S, const pmg_weights& w) {
+// ---- B200 time estimate of one group kernel (cost_model 0) ----
+// A warp walks its tile row by row (nsteps steps).  One step issues I_step warp instructions: the stage
+// bodies for V*TX points per lane plus per-stage shuffles / per-stream loads / fixed TMA+loop overhead.
+// The w warps resident on an SM share its 4 issue slots per clock, and one step cannot be shorter than the
+// row-delivery latency of a PREF-deep TMA ring.  Static tile striding gives ceil(tiles / slots) tiles to the
+// busiest warp.  The kernel cannot beat its HBM time.  Constants were fitted on B200 schedule sweeps
+// (profiles/sweep_r01_*.txt, tools/fit_weights.py).
+struct TimeModel {
+  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 800, launch_us = 1, c_border = 1.5;
+};
+static TimeModel time_model() {
+  TimeModel m;
+  if (const char* e = getenv("PMG_TM")) {     // calibration hook: "c0,c_stage,c_stream,lat_cycles,launch_us,c_border"
+    double v[6];
+    if (sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) == 6)
+      m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5]};
+  }
+  return m;
+}
+
+// instructions of a stage body per point: like ops_of, but index expressions of reads cost nothing (they are
+// resolved at compile time into registers / shuffles / shared-memory offsets)
+static double body_ops(const Expr& e) {
+  if (e.op == Expr::ACCESS) return 0;
+  double c = 0;
+  for (auto& a : e.args) c += body_ops(*a);
+  switch (e.op) {
+    case Expr::BIN:
+      if (e.text == "/") return c + (e.kind == Kind::Float ? 8 : 20);
+      if (e.text == "%") return c + 20;
+      return c + 1;
+    case Expr::UN: return c + 1;
+    case Expr::CALL:
+      if (e.text == "sqrt") return c + 8;
+      if (e.text == "lerp") return c + 3;
+      if (e.text == "clamp") return c + 2;
+      return c + 1;
+    case Expr::TABLE: return c + 4;
+    default: return c;
+  }
+}
+
+static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec& S, double resident_warps,
+                          CostBreakdown* rec = nullptr) {
+  static const TimeModel M = time_model();
+  const Pipeline& p = *A.p;
+  const KConfig& k = g.cfg;
+  const double H = (double)g.ext.e[1], W = (double)g.ext.e[2], C = (double)g.npl;
+  const double tiles = C * std::ceil(H / k.TH) * std::ceil(W / g.OW);
+  double ops = 0;
+  for (auto& P : g.gs) ops += std::max(1.0, body_ops(*p.stages[P.id].expr));
+  const double I_step = k.V * k.TX * ops + k.TX * (M.c_stage * g.gs.size() + M.c_stream * g.streams.size()) + M.c0;
+  const double R = std::max(1.0, std::floor(resident_warps));
+  const double lat = M.lat_cycles * 4.0 / std::max(1, k.PREF);
+  // border tiles (first/last tile rows, first/last tile columns) run concurrently in the border kernel, cut
+  // into TH_b-row tiles, through the general body (c_border x the instructions) at about half the residency
+  const double ntx = std::ceil(W / g.OW), nty = std::ceil(H / k.TH);
+  const double bt = C * (std::min(nty, 2.0) * ntx + std::max(0.0, nty - 2) * std::min(ntx, 2.0));
+  const double it = std::max(0.0, tiles - bt);
+  const int THb = g.TH_b > 0 ? g.TH_b : k.TH;
+  const double btb = bt * k.TH / THb, Rb = std::max(1.0, std::floor(R / 2));
+  // SM issue bound: the busiest SM issues ceil(tiles / NSMs) tiles' instructions at 4 per clock;
+  // warp latency bound: the busiest warp walks ceil(tiles / (R * NSMs)) tiles at <= 1 instruction per clock
+  // and no faster than the ring delivers rows
+  const double t_sm = (std::ceil(it / S.nsms) * g.nsteps * I_step + std::ceil(btb / S.nsms) * (THb - g.t_first) *
+                       I_step * M.c_border) / 4.0;
+  const double t_warp = std::max(std::ceil(it / (R * S.nsms)) * g.nsteps * std::max(I_step, lat),
+                                 std::ceil(btb / (Rb * S.nsms)) * (THb - g.t_first) * std::max(I_step * M.c_border, lat));
+  const double t_issue = std::max(t_sm, t_warp) / S.sm_clock_hz;
+  double bytes = 0;
+  for (auto& st : g.streams) bytes += (double)(k.TH + st.hi - st.lo) * st.row_elems * st.esz;
+  for (auto& P : g.gs)
+    if (P.materialize) bytes += (double)k.TH * g.OW * dtype_size(p.stages[P.id].dtype);
+  const double t_mem = tiles * bytes / S.gl_mem_bw;
+  if (rec) {
+    rec->tm_ops = ops; rec->tm_stages = (double)g.gs.size(); rec->tm_streams = (double)g.streams.size();
+    rec->tm_nsteps = g.nsteps; rec->tm_tiles = tiles; rec->tm_bytes = tiles * bytes; rec->tm_resident = R;
+    rec->tm_border_tiles = btb; rec->tm_border_steps = THb - g.t_first;
+  }
+  return std::max(t_issue, t_mem) * 1e6 + M.launch_us;
+}
+
+CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S, const pmg_weights& w, int cost_model) {
   const Pipeline& p = *A.p;
   const KConfig& k = g.cfg;
   CostBreakdown c;
@@ -171,12 +255,15 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
   //  extraTBs  = idle fraction of the last wave of tiles, 1 - waves / ceil(waves) (0 below one wave, where the
   //              shortfall is already in the occupancy term).
   const double slots = c.occupancy * S.max_warps_per_sm, tiles_ = c.total_threads / S.warp_size;
+  c.est_us = slots > 0 ? est_time_us(A, g, S, slots, &c) : std::numeric_limits<double>::infinity();
   if (slots > 0) {
     c.occupancy = std::min(slots, tiles_ / S.nsms) / S.max_warps_per_sm;
     const double waves = tiles_ / (slots * S.nsms);
     c.extra_tbs = waves <= 1 ? 0.0 : 1.0 - waves / std::ceil(waves);
   }
   weigh(c, w);
+  c.alg2_cost = c.cost;
+  if (cost_model == 0 && !c.infinite) c.cost = c.est_us;
   return c;
 }
 
@@ -193,7 +280,9 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
   std::vector<int> TXs = o.chunks > 0 ? std::vector<int>{o.chunks} : std::vector<int>{1, 2, 4};
   std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 64};
   std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{1, 2, 4, 8};
-  std::vector<int> PFs = o.prefetch > 0 ? std::vector<int>{o.prefetch} : std::vector<int>{4, 8};
+  // PREF: 4 rows in flight per warp is what the time model was fitted on (profiles/sweep_*); deeper rings are
+  // available through the override
+  std::vector<int> PFs = o.prefetch > 0 ? std::vector<int>{o.prefetch} : std::vector<int>{4};
   std::vector<int> TXSZ = o.tx_size > 0 ? std::vector<int>{o.tx_size} : std::vector<int>{32, 128};
   std::vector<int> Ss = o.smem_chunks >= 0 ? std::vector<int>{o.smem_chunks} : std::vector<int>{0};
   struct Cand { Group g; CostBreakdown c; };
@@ -214,7 +303,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                 cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0};
                 ++count;
                 if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
-                CostBreakdown c = b200_cost(A, cand, S, w);
+                CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model);
                 if (c.infinite) { why = c.why; continue; }
                 cands.push_back({cand, c});
               }
@@ -239,11 +328,16 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
       int regs = -1, spill = -1;
       if (!(*probe)(c.g, &regs, &spill) || regs <= 0) { fin.push_back(c); continue; }
       c.g.regs_est = regs;
-      c.c = b200_cost(A, c.g, S, w);
+      c.c = b200_cost(A, c.g, S, w, o.cost_model);
       if (spill > 0) { c.c.infinite = true; c.c.why = "register spills"; c.c.cost = std::numeric_limits<double>::infinity(); }
       fin.push_back(c);
     }
     std::sort(fin.begin(), fin.end(), better);
+    if (getenv("PMG_SCHED_TRACE"))
+      for (auto& f : fin)
+        fprintf(stderr, "[pmg sched] %zu stages V%d TX%d TH%d NW%d PF%d regs %d est %.2f cost %.4f%s\n", f.g.stages.size(),
+                f.g.cfg.V, f.g.cfg.TX, f.g.cfg.TH, f.g.cfg.NW, f.g.cfg.PREF, f.g.regs_est, f.c.est_us, f.c.cost,
+                f.c.infinite ? " (inf)" : "");
     if (!fin.empty() && !fin[0].c.infinite) {
       g = fin[0].g;
       if (out) *out = fin[0].c;
@@ -323,11 +417,52 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
   std::vector<std::pair<int, int>> segs;
   for (int j = n; j > 0; j = from[j]) segs.push_back({from[j], j});
   std::reverse(segs.begin(), segs.end());
-  sch.group_of_stage.assign(n, -1);
-  for (size_t gi = 0; gi < segs.size(); ++gi)
-    for (int q = segs[gi].first; q < segs[gi].second; ++q) sch.group_of_stage[p.topo[q]] = (int)gi;
+  auto gos_of = [&](const std::vector<std::pair<int, int>>& sg) {
+    std::vector<int> v(n, -1);
+    for (size_t gi = 0; gi < sg.size(); ++gi)
+      for (int q = sg[gi].first; q < sg[gi].second; ++q) v[p.topo[q]] = (int)gi;
+    return v;
+  };
+  // probed merge pass: the DP costs segments with the register *estimate*, which over-estimates large fused
+  // groups (the interior kernel's folds shrink them); try merging neighbours with ptxas' counts and keep a
+  // merge when the probed pipeline estimate drops
+  if (probe && *probe && fuse && segs.size() > 1) {
+    auto probed = [&](const std::vector<std::pair<int, int>>& sg, double& total) {
+      std::vector<int> gv = gos_of(sg);
+      total = 0;
+      for (auto& q : sg) {
+        Group h;
+        h.stages.assign(p.topo.begin() + q.first, p.topo.begin() + q.second);
+        CostBreakdown cb;
+        if (!best_config(A, h, gv, S, w, o, &cb, probe) || cb.infinite) return false;
+        total += cb.cost;
+      }
+      return true;
+    };
+    double cur;
+    if (probed(segs, cur)) {
+      for (bool changed = true; changed && segs.size() > 1;) {
+        changed = false;
+        for (size_t gi = 0; gi + 1 < segs.size(); ++gi) {
+          std::vector<int> merged(p.topo.begin() + segs[gi].first, p.topo.begin() + segs[gi + 1].second);
+          if (!feasible_stage_set(A, merged)) continue;
+          auto trial = segs;
+          trial[gi].second = trial[gi + 1].second;
+          trial.erase(trial.begin() + gi + 1);
+          double t;
+          if (probed(trial, t) && t < cur) {
+            segs = trial;
+            cur = t;
+            changed = true;
+            break;
+          }
+        }
+      }
+    }
+  }
+  sch.group_of_stage = gos_of(segs);
   std::ostringstream js;
-  js << "{\"mode\":\"dp\",\"total_cost\":" << best[n] << ",\"groups\":[";
+  js << "{\"mode\":\"dp\",\"dp_cost\":" << best[n] << ",\"groups\":[";
   for (size_t gi = 0; gi < segs.size(); ++gi) {
     Group g = seg_group[segs[gi].first][segs[gi].second];
     // re-select with the final grouping (materialisation depends on the other groups) and with the
@@ -368,6 +503,12 @@ std::string cost_json(const CostBreakdown& c) {
   o << ",\"unusedReg\":"; num(c.unused_reg);
   o << ",\"fracOverlap\":"; num(c.frac_overlap);
   o << ",\"extraTBs\":"; num(c.extra_tbs);
+  o << ",\"estUs\":"; num(c.est_us);
+  o << ",\"alg2Cost\":"; num(c.alg2_cost);
+  o << ",\"tm\":{\"ops\":" << c.tm_ops << ",\"stages\":" << c.tm_stages << ",\"streams\":" << c.tm_streams
+    << ",\"nsteps\":" << c.tm_nsteps << ",\"tiles\":" << c.tm_tiles << ",\"bytes\":" << c.tm_bytes
+    << ",\"resident\":" << c.tm_resident << ",\"border_tiles\":" << c.tm_border_tiles << ",\"border_steps\":"
+    << c.tm_border_steps << "}";
   o << ",\"cost\":"; num(c.cost);
   o << ",\"infinite\":" << (c.infinite ? "true" : "false") << ",\"why\":\"" << c.why << "\"}";
   return o.str();
@@ -383,7 +524,8 @@ std::string config_json(const Analysis& A, const Group& g) {
     << ",\"PREF\":" << k.PREF << ",\"txSz\":" << k.tx_size << ",\"fracReg\":" << double(k.TX - k.S) / k.TX
     << ",\"tile\":[" << k.V * k.TX << "," << k.TH << ",1],\"block\":[" << 32 * k.NW << ",1,1],\"warp\":[32,1,1]"
     << ",\"CW\":" << g.CW << ",\"OW\":" << g.OW << ",\"PL\":" << g.PL << ",\"PR\":" << g.PR << ",\"t_first\":" << g.t_first
-    << ",\"unroll\":" << g.U << ",\"warp_smem\":" << g.warp_smem << ",\"regs_est\":" << g.regs_est << ",\"stage_geom\":[";
+    << ",\"unroll\":" << g.U << ",\"warp_smem\":" << g.warp_smem << ",\"regs_est\":" << g.regs_est << ",\"state_regs\":" << interior_state_regs(A, g)
+    << ",\"stage_geom\":[";
   for (size_t i = 0; i < g.gs.size(); ++i) {
     auto& P = g.gs[i];
     o << (i ? "," : "") << "{\"stage\":\"" << p.stages[P.id].name << "\",\"hi\":" << P.hi << ",\"lo\":" << P.lo

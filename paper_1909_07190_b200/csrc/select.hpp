@@ -18,7 +18,11 @@ struct CostBreakdown {          // every term of Alg. 2
   double max_tb_per_sm = 0, sh_mem_occ = 0, reg_occ = 0, occupancy = 0;
   double warp_bw = 0, mem_time = 0, compute_time = 0;
   double unallocated_sh_mem = 0, unused_reg = 0, frac_overlap = 0, extra_tbs = 0;
-  double cost = 0;
+  double est_us = 0;            // B200 time estimate of the group kernel
+  double tm_ops = 0, tm_stages = 0, tm_streams = 0, tm_nsteps = 0, tm_tiles = 0, tm_bytes = 0, tm_resident = 0, tm_border_tiles = 0,
+         tm_border_steps = 0;
+  double alg2_cost = 0;         // the weighted seven-term sum (l.981)
+  double cost = 0;              // the ranking value: est_us (cost_model 0) or alg2_cost (cost_model 1)
   bool infinite = false;
   std::string why;
 };
@@ -30,7 +34,8 @@ bool weights_preset(const std::string& name, pmg_weights* out);
 double stage_ops(const Pipeline& p, int stage);
 
 // B200-mode Alg. 2 for a built group (KConfig -> paper symbols, DESIGN.md §"Selector")
-CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& spec, const pmg_weights& w);
+CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& spec, const pmg_weights& w,
+                        int cost_model = 0);
 
 // RegUsage(H) "measured with nvcc": compile a candidate and return ptxas' registers / spill bytes
 using RegProbe = std::function<bool(const Group& g, int* regs, int* spill_bytes)>;

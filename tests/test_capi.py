@@ -183,7 +183,7 @@ def test_dp_fusion_equals_brute_force(text):
             continue
         if best is None or r["total_cost"] < best[0] - 1e-9:
             best = (r["total_cost"], [g["config"]["stages"] for g in r["groups"]])
-    assert abs(dp["total_cost"] - best[0]) < 1e-9 * max(1.0, abs(best[0]))
+    assert abs(dp["dp_cost"] - best[0]) < 1e-9 * max(1.0, abs(best[0]))
     assert [g["config"]["stages"] for g in dp["groups"]] == best[1]
 
 

@@ -1,0 +1,115 @@
+"""Fit and check the selector's B200 time estimate (cost_model 0, select.cpp `est_time_us`) against measured
+schedule sweeps (profiles/sweep_<round>_<workload>.txt from tools/sweep.py on a B200).
+
+The host-side features of every measured configuration (body ops, stages, streams, steps, tiles, resident
+warps, bytes — the `tm` block of the cost JSON) are collected once; the model is then evaluated in numpy for
+a grid of constants.  Score = mean over workloads of log(t[pick] / t[best]), the slowdown the selector would
+cause, plus leave-one-workload-out cross-validation of the fit (the paper fits its weights by LOOCV,
+P:1158-1162).
+
+    python tools/fit_time_model.py --round r02 harris unsharp blur camera
+"""
+import argparse
+import itertools
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import paper_1909_07190_b200 as pmg  # noqa: E402
+import pmg_inputs as PI  # noqa: E402
+
+SPEC = pmg.gpu_spec("b200")
+
+
+def features(round_, name):
+    wl = PI.WORKLOADS[name]
+    pipe = pmg.Pipeline(wl.text)
+    rows = []
+    for line in open(ROOT / "profiles" / f"sweep_{round_}_{name}.txt"):
+        r = json.loads(line) if line.startswith("{") else None
+        if not r or "ms" not in r or r["spec"] == "auto":
+            continue
+        kv = {k: int(v) for k, v in (x.split("=") for x in r["spec"].split(","))}
+        s = pipe.schedule(wl.params, spec=SPEC, opts=pmg.sched_opts(**kv))
+        if len(s["groups"]) != r.get("nk", len(s["groups"])):
+            continue            # the measured run used another grouping (older selector)
+        groups = [dict(g["cost"]["tm"], V=g["config"]["V"], TX=g["config"]["TX"], PREF=g["config"]["PREF"],
+                       TH=g["config"]["TH"], t_first=g["config"]["t_first"]) for g in s["groups"]]
+        rows.append((r["spec"], r["ms"] * 1e3, groups))
+    return rows
+
+
+def est(groups, c0, c_stage, c_stream, lat, launch, c_border):
+    t = 0.0
+    for g in groups:
+        I = g["V"] * g["TX"] * g["ops"] + g["TX"] * (c_stage * g["stages"] + c_stream * g["streams"]) + c0
+        R = max(1.0, g["resident"])
+        L = lat * 4.0 / max(1, g["PREF"])
+        btb, sb = g["border_tiles"], g["border_steps"]
+        it = max(0.0, g["tiles"] - btb * (sb - (g["nsteps"] - g["TH"])) / g["TH"]) if False else None
+        bt_th = btb * (sb + g["t_first"]) / g["TH"]          # border tiles in TH units
+        it = max(0.0, g["tiles"] - bt_th)
+        Rb = max(1.0, math.floor(R / 2))
+        n = SPEC.nsms
+        t_sm = (math.ceil(it / n) * g["nsteps"] * I + math.ceil(btb / n) * sb * I * c_border) / 4.0
+        t_warp = max(math.ceil(it / (R * n)) * g["nsteps"] * max(I, L),
+                     math.ceil(btb / (Rb * n)) * sb * max(I * c_border, L))
+        t_issue = max(t_sm, t_warp) / SPEC.sm_clock_hz
+        t_mem = g["bytes"] / SPEC.gl_mem_bw
+        t += max(t_issue, t_mem) * 1e6 + launch
+    return t
+
+
+def score(data, prm):
+    out = []
+    for rows in data:
+        e = np.array([est(g, *prm) for _, _, g in rows])
+        m = np.array([t for _, t, _ in rows])
+        out.append(math.log(m[int(np.argmin(e))] / m.min()))
+    return float(np.mean(out)), out
+
+
+GRID = list(itertools.product([10, 30, 60], [2, 5, 10, 20], [0, 3], [400, 800, 1200, 1800, 2600], [1, 3], [1.5, 2, 3, 4, 6]))
+
+
+def fit(data):
+    best = None
+    for prm in GRID:
+        s, _ = score(data, prm)
+        if best is None or s < best[0] - 1e-12:
+            best = (s, prm)
+    return best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", default="r01")
+    ap.add_argument("workloads", nargs="+")
+    a = ap.parse_args()
+    data = [features(a.round, n) for n in a.workloads]
+    cur = (10, 2, 0, 800, 1, 1.5)
+    print("current constants", cur, "loss", [round(x, 3) for x in score(data, cur)[1]])
+    if len(data) > 1:
+        cv = []
+        for i in range(len(data)):
+            _, prm = fit([d for j, d in enumerate(data) if j != i])
+            cv.append(score([data[i]], prm)[0])
+        print("LOOCV held-out losses", [round(x, 3) for x in cv], "mean", round(float(np.mean(cv)), 4))
+    s, prm = fit(data)
+    print("fitted on all:", prm, "loss", round(s, 4))
+    for rows, n in zip(data, a.workloads):
+        e = np.array([est(g, *prm) for _, _, g in rows])
+        m = np.array([t for _, t, _ in rows])
+        i = int(np.argmin(e))
+        rk = lambda x: np.argsort(np.argsort(x))
+        print(f"  {n}: pick {rows[i][0]} {m[i]:.1f} us (best {m.min():.1f}); est/meas median "
+              f"{np.median(e / m):.2f}; spearman {np.corrcoef(rk(e), rk(m))[0, 1]:.3f}")
+
+
+if __name__ == "__main__":
+    main()

@@ -46,7 +46,7 @@ def main():
         specs = sys.argv[2:]
     if specs == ["grid"]:
         specs = [f"vec={v},chunks={tx},rows={th},warps={nw},prefetch={pf}"
-                 for v, tx, th, nw, pf in itertools.product([2, 4], [1, 2], [16, 32, 64], [1, 2, 4], [4])]
+                 for v, tx, th, nw, pf in itertools.product([2, 4], [1, 2], [8, 16, 24, 32, 64], [1, 2], [4])]
     inputs_np = wl.inputs()
     pipe = pmg.Pipeline(wl.text)
     px = wl.params["W"] * wl.params["H"]
