@@ -640,6 +640,7 @@ struct Emitter {
   std::string run() {
     const KConfig& k = g.cfg;
     o << "// generated by libpmg (emit.cpp) for group " << g.name << ": ";
+    if (getenv("PMG_NO_PROXY_FENCE")) o << "\n#define PMG_NO_PROXY_FENCE 1\n// ";   // timing experiment only
     for (auto& s : g.gs) o << p.stages[s.id].name << " ";
     o << "\n#include \"pmg_otpw.cuh\"\n\n";
     for (auto& P : g.gs) himax = std::max(himax, P.hi);
@@ -698,7 +699,16 @@ struct Emitter {
       Uk = g.U;
     }
     const char* dec = interior ? "pmg_tile_int" : "pmg_tile_bdr";
-    int minb = k.regcap > 0 ? std::max(1, 65536 / (k.regcap * 32 * k.NW)) : 1;
+    int cap = k.regcap;
+    if (!interior && cap <= 0) {
+      // border tiles are latency-bound and share the SMs with the interior kernel: cap their registers so
+      // that many of them stay resident
+      // measured (profiles/sweep notes in DESIGN.md): a 96-register cap helps small pipelines (unsharp 2048^2:
+      // 0.035 -> 0.027 ms) and hurts large general bodies (Harris 0.106 -> 0.120, camera 0.115 -> 0.127 ms)
+      const char* e = getenv("PMG_BORDER_REGCAP");
+      cap = e ? atoi(e) : (g.regs_est > 0 && g.regs_est <= 72 ? 96 : 0);
+    }
+    int minb = cap > 0 ? std::max(1, 65536 / (cap * 32 * k.NW)) : 1;
     o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << (interior ? "" : "_b")
       << "(const __grid_constant__ PmgArgs a) {\n";
     o << "  extern __shared__ __align__(128) char pmg_smem[];\n"
@@ -757,7 +767,7 @@ struct Emitter {
       for (size_t j = 0; j < g.streams.size(); ++j)
         o << "    pmg_bulk_g2s_if(ring_addr + s * RING + p_dst" << j << ", p_src" << j << " + (i64)pmg_clampi(p_y0 + (TFIRST + "
           << g.streams[j].hi << ") + s, 0, H - 1) * a.t[" << g.streams[j].tensor_slot << "].row_pitch, p_bytes" << j << ", bar, leader);\n";
-      o << "  }\n  int c_slot = 0;\n  u32 phase = 0u;\n";
+      o << "  }\n  int c_slot = 0;\n  u32 phase = 0u;   // parity of the ring's current lap (all slots are used round-robin)\n";
     }
     o << "  for (int it = 0; it < my_tiles; ++it) {\n"
          "    const int tile = gw + it * nwt;\n"
@@ -816,6 +826,11 @@ struct Emitter {
         int s_ = t - g.t_first + k.PREF;
         step(true, phase_of(t), true, t, s_ < g.nsteps ? 1 : 0);
       }
+      // running output row pointers of the main section and tail (row y0 + t + hi at step t = 0)
+      for (int i = 0; i < n; ++i)
+        if (g.gs[i].materialize)
+          o << "      char* optr" << i << " = obase" << i << " + (i64)(y0 + " << g.gs[i].hi << ") * a.t[" << g.gs[i].tensor_slot
+            << "].row_pitch;\n";
       // main section: the refill of every step targets this tile (pointer increment, no clamp)
       const int a_end = std::max(0, k.TH - k.PREF) / Uk * Uk;
       if (a_end > 0) {
@@ -864,9 +879,8 @@ struct Emitter {
 
   void stream_reads(int u, bool fast, const std::string& ind) {
     o << ind << "const int slq = c_slot;\n"
-      << ind << "pmg_mbar_wait(bar0 + 8 * slq, (phase >> slq) & 1u);\n"
-      << ind << "phase ^= 1u << slq;\n"
-      << ind << "c_slot = (slq + 1 == PREF) ? 0 : slq + 1;\n"
+      << ind << "pmg_mbar_wait(bar0 + 8 * slq, phase);\n"
+      << ind << "if (slq + 1 == PREF) { c_slot = 0; phase ^= 1u; } else { c_slot = slq + 1; }\n"
       << ind << "{\n" << ind << "const char* srow = ring + slq * RING;\n";
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
@@ -906,14 +920,20 @@ struct Emitter {
     std::string tt = tconst ? std::to_string(tval) : "t";
     if (rmode == 1) {
       // same tile, interior: rows need no clamp; the source pointers advance one row per step
-      o << ind << "{\n" << ind << "  const u32 bar = bar0 + 8 * slq;\n"
-        << ind << "  pmg_fence_proxy_async_if(leader);\n"
-        << ind << "  pmg_mbar_expect_tx_if(bar, p_total, leader);\n";
-      for (size_t j = 0; j < g.streams.size(); ++j) {
-        const GStream& S = g.streams[j];
-        o << ind << "  pmg_bulk_g2s_if(ring_addr + slq * RING + p_dst" << j << ", q_ptr" << j << ", p_bytes" << j << ", bar, leader);\n"
-          << ind << "  q_ptr" << j << " += a.t[" << S.tensor_slot << "].row_pitch;\n";
+      if (g.streams.size() == 1 && !getenv("PMG_NO_ELECT")) {
+        o << ind << "{\n" << ind << "  pmg_refill1_elect(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, q_ptr0, p_bytes0);\n"
+          << ind << "  q_ptr0 += a.t[" << g.streams[0].tensor_slot << "].row_pitch;\n" << ind << "}\n";
+        return;
       }
+      o << ind << "{\n" << ind << "  const u32 bar = bar0 + 8 * slq;\n"
+        << ind << "  if (leader) {\n"
+        << ind << "    pmg_fence_proxy_async();\n"
+        << ind << "    pmg_mbar_expect_tx(bar, p_total);\n";
+      for (size_t j = 0; j < g.streams.size(); ++j)
+        o << ind << "    pmg_bulk_g2s(ring_addr + slq * RING + p_dst" << j << ", q_ptr" << j << ", p_bytes" << j << ", bar);\n";
+      o << ind << "  }\n";
+      for (size_t j = 0; j < g.streams.size(); ++j)
+        o << ind << "  q_ptr" << j << " += a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
       o << ind << "}\n";
       return;
     }
@@ -927,6 +947,15 @@ struct Emitter {
       o << ind << "  const int s = " << tt << " - TFIRST + PREF;\n"
         << ind << "  const bool nx = s >= NSTEPS;\n"
         << ind << "  const int sr = nx ? s - NSTEPS : s;\n";
+    }
+    if (g.streams.size() == 1 && !getenv("PMG_NO_ELECT")) {
+      const GStream& S = g.streams[0];
+      o << ind << "  const int yq = nx ? pn_y0 : p_y0;\n"
+        << ind << "  if (!nx || has_next)\n"
+        << ind << "    pmg_refill1_elect(bar0 + 8 * slq, nx ? pn_total : p_total, ring_addr + slq * RING + (nx ? pn_dst0 : p_dst0), "
+        << "(nx ? pn_src0 : p_src0) + (i64)pmg_clampi(yq + (TFIRST + " << S.hi << ") + sr, 0, H - 1) * a.t[" << S.tensor_slot
+        << "].row_pitch, nx ? pn_bytes0 : p_bytes0);\n" << ind << "}\n";
+      return;
     }
     o << ind << "  const bool go = leader && (!nx || has_next);\n"
       << ind << "  const u32 bar = bar0 + 8 * slq;\n"
@@ -955,6 +984,26 @@ struct Emitter {
     bool check_rows = !fast || (!tconst && P.hi > 0);
     std::string T = "a.t[" + std::to_string(P.tensor_slot) + "]";
     std::string inbuf = "(unsigned)(" + rowv + " - " + T + ".row_base) < (unsigned)" + T + ".nrows";
+    if (fast && !tconst) {
+      // interior main loop / tail: running row pointer (no 64-bit multiply) and a predicated vector store
+      std::string pred = inbuf;
+      if (check_rows) pred = "(" + rowv + " < yend) && " + pred;
+      o << ind << "{\n" << ind << "  char* orow = optr" << i << ";\n" << ind << "  optr" << i << " += " << T << ".row_pitch;\n"
+        << ind << "  const bool sp = " << pred << ";\n";
+      for (int kk = 0; kk < TX; ++kk) {
+        int lo = g.PL - 32 * V * kk <= 0 ? 0 : std::min(32, (g.PL - 32 * V * kk) / V);
+        int hi = std::max(0, std::min(32, (g.CW - g.PR - 32 * V * kk) / V));
+        if (hi <= lo) continue;
+        o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
+        for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
+        o << "};\n";
+        std::string lanes = (lo == 0 && hi == 32) ? "" : " && lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi);
+        o << ind << "    pmg_stg_vec_if<" << ct << ", " << V << ">(orow + " << 32 * V * kk * esz << ", w, sp" << lanes << ");\n"
+          << ind << "  }\n";
+      }
+      o << ind << "}\n";
+      return;
+    }
     o << ind << "{\n";
     if (check_rows) o << ind << "if (" << rowv << " >= y0 && " << rowv << " < yend && " << inbuf << ") {\n";
     else o << ind << "if (" << inbuf << ") {\n";

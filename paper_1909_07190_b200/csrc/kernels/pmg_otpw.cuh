@@ -114,6 +114,39 @@ __device__ __forceinline__ void pmg_stg_vec(char* dst, const T (&v)[N]) {
   }
 }
 
+// one elected lane: proxy fence, expect_tx(total), and one bulk copy (single stream) -- one asm block so that
+// ptxas sees a single elect.sync predicate around the uniform-operand copy
+__device__ __forceinline__ void pmg_refill1_elect(u32 bar, u32 total, u32 dst, const void* src, u32 bytes) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+#ifndef PMG_NO_PROXY_FENCE
+      "@p fence.proxy.async.shared::cta;\n\t"
+#endif
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+      "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %4, [%0];\n}"
+      ::"r"(bar), "r"(total), "r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+
+// predicated vector store (no branch: the interior body stays one basic block)
+template <typename T, int N>
+__device__ __forceinline__ void pmg_stg_vec_if(char* dst, const T (&v)[N], bool p) {
+  constexpr int B = N * (int)sizeof(T);
+  PmgVec<T, N> u;
+#pragma unroll
+  for (int i = 0; i < N; ++i) u.e[i] = v[i];
+  if constexpr (B == 16)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.v4.b32 [%0], {%1, %2, %3, %4};\n}" ::"l"(dst),
+                 "r"(u.w16.x), "r"(u.w16.y), "r"(u.w16.z), "r"(u.w16.w), "r"((int)p) : "memory");
+  else if constexpr (B == 8)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.b32 [%0], {%1, %2};\n}" ::"l"(dst),
+                 "r"(u.w8.x), "r"(u.w8.y), "r"((int)p) : "memory");
+  else if constexpr (B == 4)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;\n}" ::"l"(dst), "r"(u.w4),
+                 "r"((int)p) : "memory");
+  else if (p) pmg_stg_vec<T, N>(dst, v);
+}
+
 // load N consecutive shared-memory elements (aligned) with one vector load
 template <typename T, int N>
 __device__ __forceinline__ void pmg_lds_vec(const char* src, T (&v)[N]) {

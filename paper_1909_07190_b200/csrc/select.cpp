@@ -21,7 +21,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <sstream>
+#include <tuple>
 
 namespace pmg {
 
@@ -143,7 +145,7 @@ static double min_txs(int64_t start, int64_t nbytes, int tx) {
 // busiest warp.  The kernel cannot beat its HBM time.  Constants were fitted on B200 schedule sweeps
 // (profiles/sweep_r01_*.txt, tools/fit_weights.py).
 struct TimeModel {
-  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 800, launch_us = 1, c_border = 1.5;
+  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1800, launch_us = 1, c_border = 6;
 };
 static TimeModel time_model() {
   TimeModel m;
@@ -318,26 +320,38 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
     return a.g.cfg.tx_size > b.g.cfg.tx_size;
   };
   std::sort(cands.begin(), cands.end(), better);
-  // finalists: replace the register estimate by ptxas' count (RegUsage "measured with nvcc");
-  // spilling configurations are rejected (their registers exceed MaxRegPerTh)
+  // finalists: replace the register estimate by ptxas' count (RegUsage "measured with nvcc").  The count
+  // depends on (V, TX, NW) but hardly on TH / txSz, so the best candidate of each of the first few distinct
+  // (V, TX, NW) keys is compiled and its count applied to every candidate with that key; spilling keys are
+  // rejected (their registers exceed MaxRegPerTh)
   if (probe && *probe) {
-    const size_t K = std::min<size_t>(cands.size(), 4);
-    std::vector<Cand> fin;
-    for (size_t i = 0; i < cands.size() && fin.size() < K; ++i) {
-      Cand c = cands[i];
+    const size_t KEYS = 5;
+    std::map<std::tuple<int, int, int>, std::pair<int, int>> meas;
+    for (size_t i = 0; i < cands.size() && meas.size() < KEYS; ++i) {
+      auto key = std::make_tuple(cands[i].g.cfg.V, cands[i].g.cfg.TX, cands[i].g.cfg.NW);
+      if (meas.count(key)) continue;
       int regs = -1, spill = -1;
-      if (!(*probe)(c.g, &regs, &spill) || regs <= 0) { fin.push_back(c); continue; }
-      c.g.regs_est = regs;
+      if (!(*probe)(cands[i].g, &regs, &spill) || regs <= 0) regs = -1;
+      meas[key] = {regs, spill};
+    }
+    std::vector<Cand> fin;
+    for (auto& c0 : cands) {
+      auto it = meas.find(std::make_tuple(c0.g.cfg.V, c0.g.cfg.TX, c0.g.cfg.NW));
+      if (it == meas.end() || it->second.first <= 0) continue;
+      Cand c = c0;
+      c.g.regs_est = it->second.first;
       c.c = b200_cost(A, c.g, S, w, o.cost_model);
-      if (spill > 0) { c.c.infinite = true; c.c.why = "register spills"; c.c.cost = std::numeric_limits<double>::infinity(); }
+      if (it->second.second > 0) { c.c.infinite = true; c.c.why = "register spills"; c.c.cost = std::numeric_limits<double>::infinity(); }
       fin.push_back(c);
     }
     std::sort(fin.begin(), fin.end(), better);
     if (getenv("PMG_SCHED_TRACE"))
-      for (auto& f : fin)
+      for (size_t i = 0; i < fin.size() && i < 6; ++i) {
+        auto& f = fin[i];
         fprintf(stderr, "[pmg sched] %zu stages V%d TX%d TH%d NW%d PF%d regs %d est %.2f cost %.4f%s\n", f.g.stages.size(),
                 f.g.cfg.V, f.g.cfg.TX, f.g.cfg.TH, f.g.cfg.NW, f.g.cfg.PREF, f.g.regs_est, f.c.est_us, f.c.cost,
                 f.c.infinite ? " (inf)" : "");
+      }
     if (!fin.empty() && !fin[0].c.infinite) {
       g = fin[0].g;
       if (out) *out = fin[0].c;

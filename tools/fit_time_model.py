@@ -92,7 +92,7 @@ def main():
     ap.add_argument("workloads", nargs="+")
     a = ap.parse_args()
     data = [features(a.round, n) for n in a.workloads]
-    cur = (10, 2, 0, 800, 1, 1.5)
+    cur = (10, 2, 0, 1800, 1, 6)
     print("current constants", cur, "loss", [round(x, 3) for x in score(data, cur)[1]])
     if len(data) > 1:
         cv = []

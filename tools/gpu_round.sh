@@ -5,7 +5,7 @@ tag=${1:-r}
 mkdir -p gpurun_out/$tag
 python -m pytest tests/test_gpu_parity.py tests/test_gpu_modes.py -x -q > gpurun_out/$tag/pytest_gpu.txt 2>&1; tail -2 gpurun_out/$tag/pytest_gpu.txt
 python tools/sweep.py harris vec=4,chunks=1,rows=32,warps=1,prefetch=4 > gpurun_out/$tag/auto_harris.txt 2>&1
-python tools/sweep.py unsharp vec=2,chunks=2,rows=32,warps=1,prefetch=4 > gpurun_out/$tag/auto_unsharp.txt 2>&1
+python tools/sweep.py unsharp vec=4,chunks=1,rows=32,warps=1,prefetch=4 vec=2,chunks=2,rows=24,warps=1,prefetch=4 > gpurun_out/$tag/auto_unsharp.txt 2>&1
 python tools/sweep.py camera vec=4,chunks=1,rows=16,warps=1,prefetch=4 > gpurun_out/$tag/auto_camera.txt 2>&1
 python tools/sweep.py blur > gpurun_out/$tag/auto_blur.txt 2>&1
 python tools/sweep.py local_laplacian > gpurun_out/$tag/auto_ll.txt 2>&1
