@@ -315,3 +315,21 @@ def test_golden_digests_unchanged():
     m = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(m)
     assert m.digests() == json.loads((gdir / "oracle_digests.json").read_text())
+
+
+# ------------------------------------------------------------------ demand-driven (sampled) oracle
+@pytest.mark.parametrize("wl", [PI.small("blur", 70, 50), PI.small("harris", 90, 61), PI.small("unsharp", 64, 40),
+                                PI.small("camera", 96, 64),
+                                PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005)],
+                         ids=lambda w: w.pipeline)
+def test_point_oracle_equals_whole_domain(wl):
+    """oracle/points.py restates the definition at requested points only (used at BASELINE sizes); it must
+    reproduce the whole-domain evaluation bit for bit, including corners, ragged edges and the data-dependent
+    plane index of the local Laplacian."""
+    from oracle import evaluate_points
+    inp = wl.inputs("structured") if "laplacian" in wl.pipeline else wl.inputs()
+    (key, ref), = evaluate(wl.text, wl.params, inp).items()
+    rng = np.random.default_rng(1)
+    pts = tuple(np.concatenate([rng.integers(0, n, size=40), [0, n - 1, n // 2]]) for n in ref.shape)
+    got = evaluate_points(wl.text, wl.params, inp, key, pts)
+    np.testing.assert_array_equal(got.view(np.uint8), np.ascontiguousarray(ref[pts]).view(np.uint8))
