@@ -138,6 +138,8 @@ def main():
     ap.add_argument("--workload", default="harris", choices=sorted(PI.WORKLOADS))
     ap.add_argument("--impl", default="pmg", choices=["pmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every run from the host instead of replaying captured CUDA graphs")
     ap.add_argument("--opts", default="", help="manual schedule, e.g. vec=4,chunks=1,rows=32,warps=4,prefetch=4")
     args = ap.parse_args()
     wl = PI.WORKLOADS[args.workload]
@@ -161,7 +163,7 @@ def main():
     torch.cuda.init()
     stream = torch.cuda.current_stream(dev)
 
-    opts = None
+    opts = pmg.sched_opts(bands=world) if world > 1 else None       # schedule for this rank's band size
     if args.opts:
         kv = dict(x.split("=") for x in args.opts.split(","))
         opts = pmg.sched_opts(**{k: int(v) for k, v in kv.items()})
@@ -184,12 +186,34 @@ def main():
         out_sets.append(outs)
     ws = plan.workspace()
 
-    def step(i):
+    def launch(i, st):
         ins, outs = in_sets[i % sets], out_sets[i % sets]
         if nb > 1:
-            plan.run_band(band, nb, ins, outs, ws, stream)
+            plan.run_band(band, nb, ins, outs, ws, st)
         else:
-            plan.run(ins, outs, ws, stream)
+            plan.run(ins, outs, ws, st)
+
+    # one CUDA graph per buffer set (the plan's launches, incl. the border kernel's fork/join, captured once):
+    # replaying takes the host launch path (~10-20 us per run through ctypes) off the timed loop, which
+    # matters for small bands
+    graphs = []
+    if not args.no_graph:
+        for i in range(max(3, args.warmup)):
+            launch(i, stream)
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream(dev)
+        for k in range(sets):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                launch(k, torch.cuda.current_stream(dev))
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def step(i):
+        if graphs:
+            graphs[i % sets].replay()
+        else:
+            launch(i, stream)
 
     for i in range(max(3, args.warmup)):
         step(i)
@@ -204,7 +228,7 @@ def main():
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches_per_step = plan.last_launches
+    launches_per_step = plan.last_launches       # the captured run launched the same kernels
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{dev}")
@@ -275,6 +299,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded U[0,1) image, pmg_inputs.py)",
         "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
+                   "launch": "CUDA graph replay per buffer set" if graphs else "host launches",
                    "l2": "inputs+outputs (328 MB) larger than L2 (126 MB); 2 rotating buffer sets",
                    "schedule": [g["config"] for g in desc["schedule"]["groups"]],
                    "kernels": desc["kernels"]},

@@ -118,7 +118,9 @@ typedef struct {
   int32_t regcap;       /* registers per thread cap (__launch_bounds__ min-blocks); <=0 = automatic */
   int32_t probe;        /* 1 = compile the selector's finalists to read ptxas register counts (default) */
   int32_t cost_model;   /* 0 = B200 time estimate (default); 1 = Alg. 2 weighted sum */
-  int32_t reserved[4];
+  int32_t bands;        /* runs will be row bands of 1/bands of the image (pmg_run_band): the time estimate
+                           counts the tiles of one band; <= 1 = whole image */
+  int32_t reserved[3];
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);

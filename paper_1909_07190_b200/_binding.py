@@ -60,7 +60,7 @@ class SchedOpts(C.Structure):
     _fields_ = [("group_of_stage", C.POINTER(C.c_int32)), ("vec", C.c_int32), ("chunks", C.c_int32),
                 ("smem_chunks", C.c_int32), ("rows", C.c_int32), ("warps", C.c_int32), ("prefetch", C.c_int32),
                 ("tx_size", C.c_int32), ("budget", C.c_int32), ("fuse", C.c_int32), ("regcap", C.c_int32),
-                ("probe", C.c_int32), ("cost_model", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("probe", C.c_int32), ("cost_model", C.c_int32), ("bands", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 P = C.c_void_p

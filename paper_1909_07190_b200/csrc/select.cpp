@@ -180,11 +180,11 @@ static double body_ops(const Expr& e) {
 }
 
 static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec& S, double resident_warps,
-                          CostBreakdown* rec = nullptr) {
+                          CostBreakdown* rec = nullptr, int bands = 1) {
   static const TimeModel M = time_model();
   const Pipeline& p = *A.p;
   const KConfig& k = g.cfg;
-  const double H = (double)g.ext.e[1], W = (double)g.ext.e[2], C = (double)g.npl;
+  const double H = std::ceil((double)g.ext.e[1] / std::max(1, bands)), W = (double)g.ext.e[2], C = (double)g.npl;
   const double tiles = C * std::ceil(H / k.TH) * std::ceil(W / g.OW);
   double ops = 0;
   for (auto& P : g.gs) ops += std::max(1.0, body_ops(*p.stages[P.id].expr));
@@ -219,7 +219,8 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   return std::max(t_issue, t_mem) * 1e6 + M.launch_us;
 }
 
-CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S, const pmg_weights& w, int cost_model) {
+CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S, const pmg_weights& w, int cost_model,
+                        int bands) {
   const Pipeline& p = *A.p;
   const KConfig& k = g.cfg;
   CostBreakdown c;
@@ -257,7 +258,7 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
   //  extraTBs  = idle fraction of the last wave of tiles, 1 - waves / ceil(waves) (0 below one wave, where the
   //              shortfall is already in the occupancy term).
   const double slots = c.occupancy * S.max_warps_per_sm, tiles_ = c.total_threads / S.warp_size;
-  c.est_us = slots > 0 ? est_time_us(A, g, S, slots, &c) : std::numeric_limits<double>::infinity();
+  c.est_us = slots > 0 ? est_time_us(A, g, S, slots, &c, bands) : std::numeric_limits<double>::infinity();
   if (slots > 0) {
     c.occupancy = std::min(slots, tiles_ / S.nsms) / S.max_warps_per_sm;
     const double waves = tiles_ / (slots * S.nsms);
@@ -305,7 +306,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                 cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0};
                 ++count;
                 if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
-                CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model);
+                CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model, o.bands);
                 if (c.infinite) { why = c.why; continue; }
                 cands.push_back({cand, c});
               }
@@ -340,7 +341,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
       if (it == meas.end() || it->second.first <= 0) continue;
       Cand c = c0;
       c.g.regs_est = it->second.first;
-      c.c = b200_cost(A, c.g, S, w, o.cost_model);
+      c.c = b200_cost(A, c.g, S, w, o.cost_model, o.bands);
       if (it->second.second > 0) { c.c.infinite = true; c.c.why = "register spills"; c.c.cost = std::numeric_limits<double>::infinity(); }
       fin.push_back(c);
     }
