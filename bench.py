@@ -138,6 +138,8 @@ def main():
     ap.add_argument("--workload", default="harris", choices=sorted(PI.WORKLOADS))
     ap.add_argument("--impl", default="pmg", choices=["pmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--simulate-bands", type=int, default=0,
+                    help="(single-GPU check of the N>1 path) time band N//2 of N on this GPU; value is N x bands")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every run from the host instead of replaying captured CUDA graphs")
     ap.add_argument("--opts", default="", help="manual schedule, e.g. vec=4,chunks=1,rows=32,warps=4,prefetch=4")
@@ -163,7 +165,9 @@ def main():
     torch.cuda.init()
     stream = torch.cuda.current_stream(dev)
 
-    opts = pmg.sched_opts(bands=world) if world > 1 else None       # schedule for this rank's band size
+    nb = args.simulate_bands if (world == 1 and args.simulate_bands > 1) else world
+    band = nb // 2 if nb != world else rank
+    opts = pmg.sched_opts(bands=nb) if nb > 1 else None             # schedule for this rank's band size
     if args.opts:
         kv = dict(x.split("=") for x in args.opts.split(","))
         opts = pmg.sched_opts(**{k: int(v) for k, v in kv.items()})
@@ -174,10 +178,13 @@ def main():
     inputs_np = wl.inputs()
 
     from gpu_util_bench import device_inputs
-    nb = world
-    band = rank
     o_r0, o_r1, i_r0, i_r1 = plan.band_rows(band, nb)
-    sets = 2
+    # rotating buffer sets: together at least 2x L2, so no run finds its inputs in L2 (bands are small at N>1)
+    set_bytes = sum(int(np.prod(io.shape[:-2])) * (i_r1 - i_r0) * io.shape[-1] * pmg._binding.DTYPE_SIZE[io.dtype]
+                    for io in plan.inputs if not io.is_table) + \
+        sum(int(np.prod(o.shape[:-2])) * (o_r1 - o_r0) * o.shape[-1] * pmg._binding.DTYPE_SIZE[o.dtype] for o in plan.outputs)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    sets = max(2, -(-2 * l2 // max(1, set_bytes)))
     in_sets, out_sets = [], []
     for _ in range(sets):
         ins = device_inputs(plan, inputs_np, dev, rows=(i_r0, i_r1) if nb > 1 else None)
@@ -300,7 +307,7 @@ def main():
         "data": "synthetic (seeded U[0,1) image, pmg_inputs.py)",
         "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
                    "launch": "CUDA graph replay per buffer set" if graphs else "host launches",
-                   "l2": "inputs+outputs (328 MB) larger than L2 (126 MB); 2 rotating buffer sets",
+                   "l2": f"{sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (>= 2x the {l2 / 1e6:.0f} MB L2)",
                    "schedule": [g["config"] for g in desc["schedule"]["groups"]],
                    "kernels": desc["kernels"]},
         "roofline": ({"bound": "alu", "achieved": alu_achieved, "peak": peak_alu, "unit": "Tops/s",
@@ -319,7 +326,9 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline and world == 1:
+    if nb != world:
+        line["config"]["simulated_bands"] = f"band {band} of {nb} timed on one GPU; value = whole image / band time"
+    if not args.no_cpu_baseline and world == 1 and nb == 1:
         line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line))
     if world > 1:
