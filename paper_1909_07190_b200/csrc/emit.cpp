@@ -76,6 +76,21 @@ struct Emitter {
   // shallower windows than the border kernel)
   std::vector<int> dS, dT;
   int Uk = 1;
+  bool in_interior = false;   // emitting the interior-tile kernel (hybrid smem chunks apply there only)
+
+  // hybrid tiling: stage i's window for chunk kk lives in warp-private shared memory (interior kernel,
+  // chunks kk < S, rotating windows)
+  bool hyb(int i, int kk) const {
+    if (!in_interior || kk >= g.cfg.S || !g.gs[i].smem) return false;
+    const int d = depS(i);
+    return d <= 1 || Uk % d == 0;
+  }
+  std::string hyb_ptr(int i, int sl, int kk, const std::string& elem) const {
+    const GStage& P = g.gs[i];
+    const int esz = dtype_size(p.stages[P.id].dtype);
+    return "(wsm + " + std::to_string(P.smem_off + sl * P.smem_rowb) + " + (" + std::to_string(P.smem_padl + kk * 32 * V) +
+           " + V * lane + (" + elem + ")) * " + std::to_string(esz) + ")";
+  }
   int back_shift = 0;   // set while emitting a fold segment evaluated m steps ahead of its stage row
   int depS(int i) const { return dS.empty() ? g.gs[i].depth : dS[i]; }
   int depT(int j) const { return dT.empty() ? g.streams[j].depth : dT[j]; }
@@ -306,6 +321,10 @@ struct Emitter {
       int b = P.hi - C.hi - gr.dy;
       DType dt = p.stages[P.id].dtype;
       b -= back_shift;
+      if (hyb(gr.idx, c.k))   // load type (2): the window row in shared memory, any x offset
+        return {"pmg_lds<" + std::string(ctype(dt)) + ">(" + hyb_ptr(gr.idx, slot(depS(gr.idx), b, c.u), c.k, std::to_string(c.v + gr.dx)) +
+                    ", 0)",
+                dtype_is_float(dt) ? Kind::Float : Kind::Int};
       return {sv(gr.idx, slot(depS(gr.idx), b, c.u), c.k, c.v + gr.dx), dtype_is_float(dt) ? Kind::Float : Kind::Int};
     }
     if (gr.kind == RKind::STREAM) {
@@ -698,6 +717,7 @@ struct Emitter {
       folds.assign(n, Fold{});
       Uk = g.U;
     }
+    in_interior = interior;
     const char* dec = interior ? "pmg_tile_int" : "pmg_tile_bdr";
     int cap = k.regcap;
     if (!interior && cap <= 0) {
@@ -1131,6 +1151,7 @@ struct Emitter {
       }
       // extension elements: neighbour lanes / neighbour chunks (load types (3) and (4))
       for (int kk = 0; kk < TX; ++kk) {
+        if (hyb(i, kk)) continue;   // shared-memory chunk: consumers read any offset from the smem row
         for (int e = -P.el; e < 0; ++e) {
           int q = (int)std::floor((double)e / V), ee = e - q * V;
           std::string own = sv(i, cur, kk, ee);
@@ -1145,6 +1166,21 @@ struct Emitter {
         }
       }
       if (st_paired(i)) complete_pairs('n', i, cur, P.el, P.er, in3);
+      if (hyb(i, 0)) {
+        // hybrid tiling: the smem chunks' row goes to the window slot in shared memory; the first register
+        // chunk also writes the head of its row into the right halo (reads across the S | S+1 boundary)
+        std::string ct = ctype(sd.dtype);
+        for (int kk = 0; kk < g.cfg.S; ++kk) {
+          o << in3 << "{ " << ct << " w[" << V << "] = {";
+          for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
+          o << "}; pmg_stg_vec<" << ct << ", " << V << ">(" << hyb_ptr(i, cur, kk, "0") << ", w); }\n";
+        }
+        if (g.cfg.S < TX && P.er > 0)
+          for (int v = 0; v < V; ++v)
+            o << in3 << "if (V * lane + " << v << " < " << P.er << ") *reinterpret_cast<" << ct << "*>("
+              << hyb_ptr(i, cur, g.cfg.S, std::to_string(v)) << ") = (" << ct << ")" << sv(i, cur, g.cfg.S, v) << ";\n";
+        o << in3 << "__syncwarp();\n";
+      }
       if (!fast) {
         if (PD > 1) {
           o << in3 << "if (" << rowv << " == 0) {\n";

@@ -27,7 +27,6 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   if (k.V != 1 && k.V != 2 && k.V != 4 && k.V != 8) return bad("V must be 1, 2, 4 or 8");
   if (k.TX < 1 || k.TX > 8 || k.S < 0 || k.S > k.TX || k.TH < 1 || k.NW < 1 || k.NW > 32 || k.PREF < 1 || k.PREF > 16)
     return bad("configuration out of range");
-  if (k.S != 0) return bad("shared-memory chunks (S>0) are not enabled in this build");
   const int gid = gos[g.stages[0]];
   // stage order: pipeline topological order
   std::vector<int> order;
@@ -232,6 +231,19 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   g.ring_bytes = off;
   int bar_bytes = round_up(8 * k.PREF, 16);
   g.warp_smem = g.streams.empty() ? 16 : bar_bytes + k.PREF * g.ring_bytes;
+  // hybrid tiling: the S leftmost chunks keep the windows of stages that are read with
+  // a row window or an x halo in warp-private shared memory; the other TX-S chunks keep them in registers
+  if (k.S > 0) {
+    for (auto& P : g.gs) {
+      if (P.depth <= 1 && P.el + P.er == 0) continue;
+      const int esz = dtype_size(p.stages[P.id].dtype), al = 16 / esz;
+      P.smem = true;
+      P.smem_padl = round_up(P.el, al);
+      P.smem_rowb = round_up((P.smem_padl + k.S * 32 * k.V + round_up(P.er, al)) * esz, 16);
+      P.smem_off = g.warp_smem;
+      g.warp_smem += P.depth * P.smem_rowb;
+    }
+  }
   g.block_smem = g.warp_smem * k.NW;
   if (g.block_smem > 227 * 1024) return bad("shared memory per block exceeds 227 KB");
   for (auto& P : g.gs)
@@ -242,7 +254,8 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   // register estimate: windows (+60% for temporaries / scheduling), fitted to ptxas counts on B200;
   // the selector replaces it with the real count for its finalists (compile probe)
   int win = 0;
-  for (auto& P : g.gs) win += P.depth * k.TX * (k.V + P.el + P.er);
+  for (auto& P : g.gs)
+    win += P.smem ? P.depth * (k.TX - k.S) * (k.V + P.el + P.er) + k.S * k.V : P.depth * k.TX * (k.V + P.el + P.er);
   for (auto& st : g.streams) win += st.depth * k.TX * (k.V + st.el + st.er);
   g.regs_est = 40 + (win * 8 + 4) / 5;
   g.why_infeasible.clear();

@@ -56,6 +56,8 @@ struct GStage {
   bool smem = false;          // hybrid: window kept in shared memory for the S smem chunks
   int tensor_slot = -1;
   int smem_off = 0;           // per-warp byte offset of its smem window (S > 0)
+  int smem_padl = 0;          // elements before column 0 of the smem row (left halo, 16-byte aligned)
+  int smem_rowb = 0;          // bytes per smem row (one window slot)
 };
 
 enum class RKind { STAGE, STREAM, GATHER };

@@ -231,7 +231,8 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
   c.tb_per_sm = tiles / k.NW / S.nsms;                                                                         // l.939
   c.sh_mem_per_tb = g.block_smem;                                                                              // l.942-943
   c.reg_tile = 0;
-  c.reg_per_th = g.regs_est;                                                                                   // l.960
+  // l.960; an estimate above the limit is clipped: ptxas caps the count (and spills), which the probe detects
+  c.reg_per_th = std::min<double>(g.regs_est, S.max_regs_per_thread);
   // global transactions per warp tile: TMA row copies of every stream + gathers + output rows
   double txs = 0;
   for (auto& st : g.streams) {

@@ -66,6 +66,20 @@ def test_schedule_invariance(name, cfg):
     check(name, 211, 77, opts=pmg.sched_opts(**cfg, tx_size=32))
 
 
+HYBRID = [dict(vec=4, chunks=2, smem_chunks=1, rows=16, warps=1, prefetch=4),
+          dict(vec=2, chunks=4, smem_chunks=2, rows=8, warps=2, prefetch=3),
+          dict(vec=4, chunks=1, smem_chunks=1, rows=32, warps=1, prefetch=4),
+          dict(vec=1, chunks=2, smem_chunks=2, rows=5, warps=4, prefetch=2)]
+
+
+@pytest.mark.parametrize("cfg", HYBRID, ids=lambda c: "V{vec}TX{chunks}S{smem_chunks}TH{rows}".format(**c))
+@pytest.mark.parametrize("name", ["blur", "harris", "unsharp", "camera"])
+def test_hybrid_tiling_parity(name, cfg):
+    """Hybrid tiling (P:645-654): the S leftmost chunks keep their stage windows in shared memory, the rest in
+    registers; the result must not change (interior kernel; border tiles stay in registers)."""
+    check(name, 1200, 131, opts=pmg.sched_opts(**cfg, tx_size=32))   # wide enough for interior tiles
+
+
 @pytest.mark.parametrize("name", ["blur", "harris", "unsharp"])
 def test_unfused_equals_fused(name):
     """One kernel per stage (every intermediate through HBM) == the fused group."""
