@@ -196,6 +196,17 @@ pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams
 pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, int nin, const pmg_buf* out,
                         int nout, void* workspace, void* stream);
 
+/* end-to-end run from host memory (the bench's e2e path): host_in / host_out are host images in the
+ * pmg_buf layout (pinned memory gives asynchronous copies); dev_in / dev_out are caller-owned full-size
+ * device staging buffers (16-byte aligned pitches).  The image is cut into `chunks` row bands (1..64,
+ * pmg_band_rows geometry): band b's new input rows are copied in on a plan-owned copy-in stream, band b
+ * runs on `stream`, and its output rows are copied out on a plan-owned copy-out stream, so the copies of
+ * neighbouring bands overlap each other and the compute.  Every input row is copied once; tables are
+ * copied whole first.  Stream-ordered: everything completes before later work on `stream`; the host
+ * buffers must stay valid until then.  Input images must have the liveouts' row extent. */
+pmg_status pmg_run_host(pmg_plan plan, const pmg_buf* host_in, int nin, const pmg_buf* host_out, int nout,
+                        const pmg_buf* dev_in, const pmg_buf* dev_out, void* workspace, int chunks, void* stream);
+
 /* device self-test of the warp-shuffle semantics of Fig. 1: lane 0 receives the sum */
 pmg_status pmg_selftest_shuffle(int device, int32_t* lane0_sum);
 

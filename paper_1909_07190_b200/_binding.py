@@ -105,6 +105,8 @@ _sig = {
                                      C.c_int, C.c_int, I64P, I64P, I64P, I64P]),
     "pmg_run_band": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.c_void_p,
                                C.c_void_p]),
+    "pmg_run_host": (C.c_int, [P, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.POINTER(Buf),
+                               C.c_void_p, C.c_int, C.c_void_p]),
     "pmg_selftest_shuffle": (C.c_int, [C.c_int, C.POINTER(C.c_int32)]),
 }
 for _name, (_res, _args) in _sig.items():

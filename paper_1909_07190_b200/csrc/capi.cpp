@@ -391,4 +391,13 @@ pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, 
   })
 }
 
+pmg_status pmg_run_host(pmg_plan plan, const pmg_buf* host_in, int nin, const pmg_buf* host_out, int nout,
+                        const pmg_buf* dev_in, const pmg_buf* dev_out, void* workspace, int chunks, void* stream) {
+  if (!plan || !host_in || !host_out || !dev_in || !dev_out || chunks < 1) return fail(PMG_ERR_ARG, "bad argument");
+  PMG_TRY({
+    plan_run_host(*plan->plan, host_in, nin, host_out, nout, dev_in, dev_out, workspace, chunks, (CUstream)stream);
+    return PMG_OK;
+  })
+}
+
 }  // extern "C"

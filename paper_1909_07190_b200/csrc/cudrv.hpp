@@ -41,6 +41,8 @@ struct Drv {
   CUresult (*EventDestroy)(CUevent);
   CUresult (*EventRecord)(CUevent, CUstream);
   CUresult (*StreamWaitEvent)(CUstream, CUevent, unsigned);
+  CUresult (*Memcpy2DAsync)(const CUDA_MEMCPY2D*, CUstream);
+  CUresult (*MemcpyHtoDAsync)(CUdeviceptr, const void*, size_t, CUstream);
 };
 
 inline Drv& drv() {
@@ -85,6 +87,8 @@ inline Drv& drv() {
     PMG_SYM(EventDestroy, "cuEventDestroy_v2");
     PMG_SYM(EventRecord, "cuEventRecord");
     PMG_SYM(StreamWaitEvent, "cuStreamWaitEvent");
+    PMG_SYM(Memcpy2DAsync, "cuMemcpy2DAsync_v2");
+    PMG_SYM(MemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2");
 #undef PMG_SYM
     if (!all) { d.err = "CUDA driver is missing required symbols"; return; }
     CUresult r = d.Init(0);

@@ -265,6 +265,12 @@ void plan_destroy(Plan* P) {
     if (P->side) drv().StreamDestroy(P->side);
     if (P->ev_fork) drv().EventDestroy(P->ev_fork);
     if (P->ev_join) drv().EventDestroy(P->ev_join);
+    if (P->h2d) drv().StreamDestroy(P->h2d);
+    if (P->d2h) drv().StreamDestroy(P->d2h);
+    for (CUevent e : P->ev_in) drv().EventDestroy(e);
+    for (CUevent e : P->ev_done) drv().EventDestroy(e);
+    if (P->ev_start) drv().EventDestroy(P->ev_start);
+    if (P->ev_end) drv().EventDestroy(P->ev_end);
     CUdevice dev;
     if (drv().DeviceGet(&dev, P->device) == CUDA_SUCCESS) drv().DevicePrimaryCtxRelease(dev);
   }
@@ -484,6 +490,103 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     (void)ntiles;
 
   }
+}
+
+}  // namespace pmg
+
+namespace pmg {
+
+// ------------------------------------------------------------------------------- host-buffer runs
+// The end-to-end path of one pipeline run from host memory: the image is cut into `chunks` row bands
+// (pmg_band_rows geometry); band b's new input rows go host->device on the copy-in stream, band b is
+// computed on the caller's stream (pmg_run_band), and its output rows go device->host on the copy-out
+// stream, so copies of one band overlap the copies and the compute of its neighbours.  Every input row is
+// copied once (bands share their halo rows in the full-size device buffer).
+void plan_run_host(Plan& P, const pmg_buf* hin, int nin, const pmg_buf* hout, int nout, const pmg_buf* din,
+                   const pmg_buf* dout, void* ws, int chunks, CUstream s) {
+  Drv& D = drv();
+  if (!D.ok) throw Error(-6, D.err);
+  const Pipeline& p = *P.pipe;
+  const Analysis& A = P.A;
+  if (nin != P.nimages + P.ntables) throw Error(-9, "expected " + std::to_string(P.nimages + P.ntables) + " inputs");
+  if (nout != P.nout) throw Error(-9, "expected " + std::to_string(P.nout) + " outputs");
+  const int64_t H = A.stage_ext[p.liveouts[0]].e[1];
+  chunks = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)chunks, H, 64}));
+  for (int i = 0; i < P.nimages; ++i)
+    if (A.image_ext[i].e[1] != H) throw Error(-9, "host runs need input images with the liveouts' row extent");
+  if (!P.h2d) {
+    check(D.StreamCreate(&P.h2d, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    check(D.StreamCreate(&P.d2h, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    check(D.EventCreate(&P.ev_start, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    check(D.EventCreate(&P.ev_end, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  }
+  while ((int)P.ev_in.size() < chunks) {
+    CUevent a, b;
+    check(D.EventCreate(&a, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    check(D.EventCreate(&b, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    P.ev_in.push_back(a);
+    P.ev_done.push_back(b);
+  }
+  auto copy2d = [&](const pmg_buf& src, bool src_host, const pmg_buf& dst, int64_t plane, int64_t r0, int64_t r1,
+                    int64_t wbytes, CUstream st) {
+    if (r1 <= r0) return;
+    CUDA_MEMCPY2D c;
+    std::memset(&c, 0, sizeof c);
+    const char* sp = (const char*)src.ptr + plane * src.plane_pitch_bytes + r0 * src.row_pitch_bytes;
+    char* dp = (char*)dst.ptr + plane * dst.plane_pitch_bytes + r0 * dst.row_pitch_bytes;
+    if (src_host) {
+      c.srcMemoryType = CU_MEMORYTYPE_HOST; c.srcHost = sp;
+      c.dstMemoryType = CU_MEMORYTYPE_DEVICE; c.dstDevice = (CUdeviceptr)(uintptr_t)dp;
+    } else {
+      c.srcMemoryType = CU_MEMORYTYPE_DEVICE; c.srcDevice = (CUdeviceptr)(uintptr_t)sp;
+      c.dstMemoryType = CU_MEMORYTYPE_HOST; c.dstHost = dp;
+    }
+    c.srcPitch = (size_t)src.row_pitch_bytes;
+    c.dstPitch = (size_t)dst.row_pitch_bytes;
+    c.WidthInBytes = (size_t)wbytes;
+    c.Height = (size_t)(r1 - r0);
+    check(D.Memcpy2DAsync(&c, st), "cuMemcpy2DAsync");
+  };
+  check(D.EventRecord(P.ev_start, s), "cuEventRecord");
+  check(D.StreamWaitEvent(P.h2d, P.ev_start, 0), "cuStreamWaitEvent");
+  check(D.StreamWaitEvent(P.d2h, P.ev_start, 0), "cuStreamWaitEvent");
+  for (int t = 0; t < P.ntables; ++t) {
+    const int ti = P.nimages + t;
+    const size_t bytes = (size_t)A.table_len[t] * dtype_size(p.tables[t].dtype);
+    check(D.MemcpyHtoDAsync((CUdeviceptr)(uintptr_t)din[ti].ptr, hin[ti].ptr, bytes, P.h2d), "cuMemcpyHtoDAsync");
+  }
+  std::vector<int64_t> copied(P.nimages, 0);
+  std::vector<pmg_buf> bin(nin), bout(nout);
+  for (int b = 0; b < chunks; ++b) {
+    BandRows br = band_rows(P, b, chunks);
+    for (int i = 0; i < P.nimages; ++i) {
+      const Ext3& e = A.image_ext[i];
+      const int64_t planes = e.has[0] ? e.e[0] : 1, wbytes = e.e[2] * dtype_size(p.images[i].dtype);
+      const int64_t r0 = std::max(copied[i], br.in_r0);
+      for (int64_t pl = 0; pl < planes; ++pl) copy2d(hin[i], true, din[i], pl, r0, br.in_r1, wbytes, P.h2d);
+      copied[i] = std::max(copied[i], br.in_r1);
+      bin[i] = din[i];
+      bin[i].ptr = (char*)din[i].ptr + br.in_r0 * din[i].row_pitch_bytes;
+    }
+    for (int t = 0; t < P.ntables; ++t) bin[P.nimages + t] = din[P.nimages + t];
+    for (int o = 0; o < nout; ++o) {
+      bout[o] = dout[o];
+      bout[o].ptr = (char*)dout[o].ptr + br.out_r0 * dout[o].row_pitch_bytes;
+    }
+    check(D.EventRecord(P.ev_in[b], P.h2d), "cuEventRecord");
+    check(D.StreamWaitEvent(s, P.ev_in[b], 0), "cuStreamWaitEvent");
+    plan_run(P, bin.data(), nin, bout.data(), nout, ws, s, chunks > 1 ? b : -1, chunks, 1, nullptr, nullptr);
+    check(D.EventRecord(P.ev_done[b], s), "cuEventRecord");
+    check(D.StreamWaitEvent(P.d2h, P.ev_done[b], 0), "cuStreamWaitEvent");
+    for (int o = 0; o < nout; ++o) {
+      const int id = p.liveouts[o];
+      const Ext3& e = A.stage_ext[id];
+      const int64_t planes = e.has[0] ? e.e[0] : 1, wbytes = e.e[2] * dtype_size(p.stages[id].dtype);
+      for (int64_t pl = 0; pl < planes; ++pl) copy2d(dout[o], false, hout[o], pl, br.out_r0, br.out_r1, wbytes, P.d2h);
+    }
+  }
+  check(D.EventRecord(P.ev_end, P.d2h), "cuEventRecord");
+  check(D.StreamWaitEvent(s, P.ev_end, 0), "cuStreamWaitEvent");
 }
 
 }  // namespace pmg

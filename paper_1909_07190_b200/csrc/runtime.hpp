@@ -54,6 +54,10 @@ struct Plan {
   CUevent ev_fork = nullptr, ev_join = nullptr;
   std::string json;
   int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
+  // host-buffer runs (pmg_run_host): copy streams and per-chunk events, created on first use
+  CUstream h2d = nullptr, d2h = nullptr;
+  std::vector<CUevent> ev_in, ev_done;
+  CUevent ev_start = nullptr, ev_end = nullptr;
 };
 
 std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,
@@ -66,6 +70,10 @@ BandRows band_rows(const Plan& P, int band, int nbands);
 // launch every group kernel; band < 0: full image; nframes >= 1 (batch)
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace, CUstream s,
               int band, int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs);
+
+// host buffers in and out, pipelined in `chunks` row bands over copy-in / compute / copy-out streams
+void plan_run_host(Plan& P, const pmg_buf* hin, int nin, const pmg_buf* hout, int nout, const pmg_buf* din,
+                   const pmg_buf* dout, void* workspace, int chunks, CUstream s);
 
 std::string kernel_dir();   // directory of libpmg.so (for the cubin cache)
 

@@ -277,6 +277,20 @@ class Plan:
         return outputs
 
 
+    def run_host(self, host_inputs, host_outputs, dev_inputs, dev_outputs, chunks: int = 8, workspace=None,
+                 stream=None):
+        """End-to-end run from host tensors (pinned CPU tensors for asynchronous copies) through full-size device
+        staging tensors; `chunks` row bands pipeline copy-in, compute and copy-out (pmg_run_host)."""
+        hi = (B.Buf * max(1, len(host_inputs)))(*[_buf(t) for t in host_inputs])
+        ho = (B.Buf * max(1, len(host_outputs)))(*[_buf(t) for t in host_outputs])
+        di = (B.Buf * max(1, len(dev_inputs)))(*[_buf(t) for t in dev_inputs])
+        do = (B.Buf * max(1, len(dev_outputs)))(*[_buf(t) for t in dev_outputs])
+        ws = workspace if workspace is not None else self.workspace()
+        B.check(B.lib.pmg_run_host(self._h, hi, len(host_inputs), ho, len(host_outputs), di, do,
+                                   C.c_void_p(ws.data_ptr()), int(chunks), self._stream(stream)))
+        return host_outputs
+
+
 def selftest_shuffle(device: int = 0) -> int:
     v = C.c_int32(-1)
     B.check(B.lib.pmg_selftest_shuffle(device, C.byref(v)))
