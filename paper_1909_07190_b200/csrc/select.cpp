@@ -145,14 +145,14 @@ static double min_txs(int64_t start, int64_t nbytes, int tx) {
 // busiest warp.  The kernel cannot beat its HBM time.  Constants were fitted on B200 schedule sweeps
 // (profiles/sweep_r01_*.txt, tools/fit_weights.py).
 struct TimeModel {
-  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1800, launch_us = 1, c_border = 6;
+  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1800, launch_us = 1, c_border = 3, cpi_warp = 4;
 };
 static TimeModel time_model() {
   TimeModel m;
-  if (const char* e = getenv("PMG_TM")) {     // calibration hook: "c0,c_stage,c_stream,lat_cycles,launch_us,c_border"
-    double v[6];
-    if (sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) == 6)
-      m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5]};
+  if (const char* e = getenv("PMG_TM")) {     // calibration hook: "c0,c_stage,c_stream,lat_cycles,launch_us,c_border,cpi_warp"
+    double v[7];
+    if (sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6]) == 7)
+      m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5], v[6]};
   }
   return m;
 }
@@ -203,8 +203,9 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   // and no faster than the ring delivers rows
   const double t_sm = (std::ceil(it / S.nsms) * g.nsteps * I_step + std::ceil(btb / S.nsms) * (THb - g.t_first) *
                        I_step * M.c_border) / 4.0;
-  const double t_warp = std::max(std::ceil(it / (R * S.nsms)) * g.nsteps * std::max(I_step, lat),
-                                 std::ceil(btb / (Rb * S.nsms)) * (THb - g.t_first) * std::max(I_step * M.c_border, lat));
+  const double t_warp = std::max(std::ceil(it / (R * S.nsms)) * g.nsteps * std::max(I_step * M.cpi_warp, lat),
+                                 std::ceil(btb / (Rb * S.nsms)) * (THb - g.t_first) *
+                                     std::max(I_step * M.c_border * M.cpi_warp, lat));
   const double t_issue = std::max(t_sm, t_warp) / S.sm_clock_hz;
   double bytes = 0;
   for (auto& st : g.streams) bytes += (double)(k.TH + st.hi - st.lo) * st.row_elems * st.esz;
@@ -283,7 +284,9 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
   std::vector<int> Vs = o.vec > 0 ? std::vector<int>{o.vec} : std::vector<int>{1, 2, 4};
   std::vector<int> TXs = o.chunks > 0 ? std::vector<int>{o.chunks} : std::vector<int>{1, 2, 4};
   std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 64};
-  std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{1, 2, 4, 8};
+  // NW: OTPW warps are independent, so the block size only sets the register budget ptxas plans for; one warp
+  // per block was fastest or tied in every B200 sweep (profiles/sweep_r05_*), larger blocks via the override
+  std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{1};
   // PREF: 4 rows in flight per warp is what the time model was fitted on (profiles/sweep_*); deeper rings are
   // available through the override
   std::vector<int> PFs = o.prefetch > 0 ? std::vector<int>{o.prefetch} : std::vector<int>{4};
@@ -327,7 +330,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
   // (V, TX, NW) keys is compiled and its count applied to every candidate with that key; spilling keys are
   // rejected (their registers exceed MaxRegPerTh)
   if (probe && *probe) {
-    const size_t KEYS = 5;
+    const size_t KEYS = 6;
     std::map<std::tuple<int, int, int>, std::pair<int, int>> meas;
     for (size_t i = 0; i < cands.size() && meas.size() < KEYS; ++i) {
       auto key = std::make_tuple(cands[i].g.cfg.V, cands[i].g.cfg.TX, cands[i].g.cfg.NW);

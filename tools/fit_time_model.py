@@ -44,7 +44,7 @@ def features(round_, name):
     return rows
 
 
-def est(groups, c0, c_stage, c_stream, lat, launch, c_border):
+def est(groups, c0, c_stage, c_stream, lat, launch, c_border, cpi=1.0):
     t = 0.0
     for g in groups:
         I = g["V"] * g["TX"] * g["ops"] + g["TX"] * (c_stage * g["stages"] + c_stream * g["streams"]) + c0
@@ -57,8 +57,8 @@ def est(groups, c0, c_stage, c_stream, lat, launch, c_border):
         Rb = max(1.0, math.floor(R / 2))
         n = SPEC.nsms
         t_sm = (math.ceil(it / n) * g["nsteps"] * I + math.ceil(btb / n) * sb * I * c_border) / 4.0
-        t_warp = max(math.ceil(it / (R * n)) * g["nsteps"] * max(I, L),
-                     math.ceil(btb / (Rb * n)) * sb * max(I * c_border, L))
+        t_warp = max(math.ceil(it / (R * n)) * g["nsteps"] * max(I * cpi, L),
+                     math.ceil(btb / (Rb * n)) * sb * max(I * c_border * cpi, L))
         t_issue = max(t_sm, t_warp) / SPEC.sm_clock_hz
         t_mem = g["bytes"] / SPEC.gl_mem_bw
         t += max(t_issue, t_mem) * 1e6 + launch
@@ -74,7 +74,7 @@ def score(data, prm):
     return float(np.mean(out)), out
 
 
-GRID = list(itertools.product([10, 30, 60], [2, 5, 10, 20], [0, 3], [400, 800, 1200, 1800, 2600], [1, 3], [1.5, 2, 3, 4, 6]))
+GRID = list(itertools.product([10, 30], [2, 5, 10], [0], [800, 1800, 2600], [1], [1.5, 3, 6], [1, 2, 3, 4, 5, 6]))
 
 
 def fit(data):
@@ -92,7 +92,7 @@ def main():
     ap.add_argument("workloads", nargs="+")
     a = ap.parse_args()
     data = [features(a.round, n) for n in a.workloads]
-    cur = (10, 2, 0, 1800, 1, 6)
+    cur = (10, 2, 0, 1800, 1, 3, 4)
     print("current constants", cur, "loss", [round(x, 3) for x in score(data, cur)[1]])
     if len(data) > 1:
         cv = []
