@@ -566,8 +566,9 @@ struct Emitter {
     // opt-in (PMG_PACK=1): bit-exact, but on B200 the make_float2 MOVs cost what the packed FADD2s save
     // (harris 6400^2: 0.1198 ms packed vs 0.1169 ms scalar)
     const char* e = getenv("PMG_PACK");
-    return V >= 2 && V % 2 == 0 && e && e[0] == '1' && !pair_on();
+    return V >= 2 && V % 2 == 0 && e && (e[0] == '1' || e[0] == '2') && !pair_on();
   }
+  bool pack_stages() const { const char* e = getenv("PMG_PACK"); return pack_on() && e[0] == '1'; }   // '2': folds only
 
   // packed fold segment: statement per spine op; pairs (v, v + V/2) of the same lane
   void fold_segment_pair(int i, int j, int u, int cur, const std::string& ind) {
@@ -1117,7 +1118,7 @@ struct Emitter {
         // consumes the carried prefix first
         if (pack_on()) fold_segment_pair(i, (int)folds[i].m.size() - 1, u, cur, in3);
         else fold_segment(i, (int)folds[i].m.size() - 1, u, cur, in3);
-      } else if (fast && pack_on() && sd.dtype == DType::F32 && pairable(*sd.expr)) {
+      } else if (fast && pack_stages() && sd.dtype == DType::F32 && pairable(*sd.expr)) {
         for (int kk = 0; kk < TX; ++kk)
           for (int v = 0; v < V / 2; ++v)
             o << in3 << "{ const float2 pv = " << pack(ex2(*sd.expr, i, kk, v, v + V / 2, u)) << "; " << sv(i, cur, kk, v)
