@@ -120,7 +120,9 @@ typedef struct {
   int32_t cost_model;   /* 0 = B200 time estimate (default); 1 = Alg. 2 weighted sum */
   int32_t bands;        /* runs will be row bands of 1/bands of the image (pmg_run_band): the time estimate
                            counts the tiles of one band; <= 1 = whole image */
-  int32_t reserved[3];
+  int32_t no_inline;    /* 0 (default): substitute data-expanding intermediate stages into their readers
+                           (a B200 option outside the paper); 1: schedule the text as written */
+  int32_t reserved[2];
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);
@@ -151,6 +153,10 @@ void pmg_sched_opts_default(pmg_sched_opts* o);
  * pmg_schedule: fusion grouping + per-group configuration with every Alg. 2 term, as JSON.
  * pmg_analyze_group: the paper's §4 geometry and Alg. 2 for one explicit group and configuration
  * (paper notation: tile T, block B, fracReg, txSz); used to pin the worked examples of §3/§4.        */
+/* the pipeline text after substituting data-expanding intermediate stages into their readers (what plans
+ * schedule unless sched_opts.no_inline): JSON {"inlined": [names], "text": "..."} */
+pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap,
+                                size_t* needed);
 pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
                         const pmg_weights* w, const pmg_sched_opts* opts, char* json, size_t cap, size_t* needed);
 pmg_status pmg_analyze_group(pmg_pipeline p, const int64_t* params, int nparams, const char* stages_csv,

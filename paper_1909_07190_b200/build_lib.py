@@ -14,7 +14,8 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 LIB = HERE / "libpmg.so"
-SOURCES = ["parse.cpp", "analysis.cpp", "group.cpp", "emit.cpp", "select.cpp", "runtime.cpp", "capi.cpp", "selftest.cpp"]
+SOURCES = ["parse.cpp", "analysis.cpp", "inline.cpp", "group.cpp", "emit.cpp", "select.cpp", "runtime.cpp", "capi.cpp",
+           "selftest.cpp"]
 
 
 def embed_header() -> Path:

@@ -2,6 +2,7 @@
 // 558-623; §5 right hyperplanes lines 645-654) and the B200 schedule/kernel description consumed by the
 // emitter and the selector.
 #pragma once
+#include <memory>
 #include <array>
 #include <string>
 #include <vector>
@@ -42,6 +43,11 @@ Analysis analyze(const Pipeline& p, const std::vector<int64_t>& params);   // th
 
 // JSON description of the dependence vectors / footprints of every edge
 std::string describe_pipeline(const Analysis& A);
+
+// inline.cpp: substitute data-expanding intermediate stages into their readers (returns the rewritten
+// pipeline; names of the inlined stages appended to *inlined)
+std::shared_ptr<Pipeline> inline_expanding(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
+                                           std::vector<std::string>* inlined);
 
 // ---- paper §4 formulas (warp geometry, scratchpads, overlap) ----
 std::array<int, 3> warp_sizes(const std::array<int, 3>& B, int warp_size);

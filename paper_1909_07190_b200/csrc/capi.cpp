@@ -1,6 +1,7 @@
 // capi.cpp — extern "C" entry points of include/pmg.h; thread-local error messages; no exceptions cross
 // the ABI.
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "../../include/pmg.h"
@@ -134,6 +135,25 @@ pmg_status pmg_pipeline_describe(pmg_pipeline p, const int64_t* params, int npar
   })
 }
 
+pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap, size_t* needed) {
+  if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
+  PMG_TRY({
+    std::vector<std::string> names;
+    auto q = inline_expanding(p->p, pvec(params, nparams), &names);
+    std::ostringstream o;
+    o << "{\"inlined\":[";
+    for (size_t i = 0; i < names.size(); ++i) o << (i ? "," : "") << "\"" << names[i] << "\"";
+    o << "],\"text\":\"";
+    for (char c : q->source) {
+      if (c == '\n') o << "\\n";
+      else if (c == '"' || c == '\\') o << '\\' << c;
+      else o << c;
+    }
+    o << "\"}";
+    return put_json(o.str(), buf, cap, needed);
+  })
+}
+
 pmg_status pmg_gpu_spec_preset(const char* name, pmg_gpu_spec* out) {
   if (!name || !out) return fail(PMG_ERR_ARG, "NULL argument");
   if (!gpu_preset(name, out)) return fail(PMG_ERR_ARG, std::string("unknown GPU preset '") + name + "'");
@@ -185,6 +205,13 @@ void pmg_sched_opts_default(pmg_sched_opts* o) {
   o->probe = 1;
 }
 
+// the pipeline the schedule works on: data-expanding stages substituted into their readers unless disabled
+static std::shared_ptr<Pipeline> effective(const std::shared_ptr<Pipeline>& p, const std::vector<int64_t>& params,
+                                           const pmg_sched_opts* opts) {
+  if (opts && opts->no_inline) return p;
+  return inline_expanding(p, params, nullptr);
+}
+
 static void spec_or_default(const pmg_gpu_spec* s, const pmg_weights* w, pmg_gpu_spec& S, pmg_weights& W) {
   if (s) S = *s;
   else gpu_preset("b200", &S);
@@ -196,7 +223,8 @@ pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, cons
                         const pmg_sched_opts* opts, char* json, size_t cap, size_t* needed) {
   if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
   PMG_TRY({
-    Analysis A = analyze(*p->p, pvec(params, nparams));
+    auto eff = effective(p->p, pvec(params, nparams), opts);
+    Analysis A = analyze(*eff, pvec(params, nparams));
     pmg_gpu_spec S;
     pmg_weights W;
     spec_or_default(spec, w, S, W);
@@ -245,7 +273,8 @@ pmg_status pmg_emit(pmg_pipeline p, const int64_t* params, int nparams, const pm
                     const pmg_sched_opts* opts, char* json, size_t cap, size_t* needed) {
   if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
   PMG_TRY({
-    Analysis A = analyze(*p->p, pvec(params, nparams));
+    auto eff = effective(p->p, pvec(params, nparams), opts);
+    Analysis A = analyze(*eff, pvec(params, nparams));
     pmg_gpu_spec S;
     pmg_weights W;
     spec_or_default(spec, w, S, W);
@@ -276,7 +305,8 @@ pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, co
   if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
   PMG_TRY({
     if (out_dir && *out_dir) setenv("PMG_CACHE_DIR", out_dir, 1);
-    Analysis A = analyze(*p->p, pvec(params, nparams));
+    auto eff = effective(p->p, pvec(params, nparams), opts);
+    Analysis A = analyze(*eff, pvec(params, nparams));
     pmg_gpu_spec S;
     pmg_weights W;
     spec_or_default(spec, w, S, W);
@@ -364,8 +394,8 @@ pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams
   if (!p || nbands < 1 || band < 0 || band >= nbands) return fail(PMG_ERR_ARG, "bad band");
   PMG_TRY({
     Plan P;
-    P.pipe = p->p;
-    P.A = analyze(*p->p, pvec(params, nparams));
+    P.pipe = effective(p->p, pvec(params, nparams), opts);
+    P.A = analyze(*P.pipe, pvec(params, nparams));
     pmg_gpu_spec S;
     pmg_weights W;
     spec_or_default(spec, w, S, W);

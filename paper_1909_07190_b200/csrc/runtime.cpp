@@ -172,6 +172,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   Drv& D = drv();
   if (!D.ok) throw Error(-6, D.err);
   auto P = std::make_unique<Plan>();
+  if (!(opts && opts->no_inline)) p = inline_expanding(p, params, &P->inlined);
   P->pipe = p;
   P->A = analyze(*p, params);
   P->device = device;
@@ -225,7 +226,9 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   P->ws_bytes = off;
   // compile + load
   std::ostringstream js;
-  js << "{\"schedule\":" << P->sch.json << ",\"kernels\":[";
+  js << "{\"inlined\":[";
+  for (size_t i = 0; i < P->inlined.size(); ++i) js << (i ? "," : "") << "\"" << P->inlined[i] << "\"";
+  js << "],\"schedule\":" << P->sch.json << ",\"kernels\":[";
   for (size_t gi = 0; gi < P->sch.groups.size(); ++gi) {
     Group& g = P->sch.groups[gi];
     g.source = emit_group(P->A, g);

@@ -53,6 +53,7 @@ struct Plan {
   CUstream side = nullptr;                 // border-tile kernels run here, forked/joined with events
   CUevent ev_fork = nullptr, ev_join = nullptr;
   std::string json;
+  std::vector<std::string> inlined;        // stages substituted into their readers (inline.cpp)
   int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
   // host-buffer runs (pmg_run_host): copy streams and per-chunk events, created on first use
   CUstream h2d = nullptr, d2h = nullptr;

@@ -273,3 +273,24 @@ def test_nvrtc_sm100a_sass_census(tmp_path):
     sass = subprocess.run(["cuobjdump", "-sass", str(cubins[0])], capture_output=True, text=True).stdout
     assert "UBLKCP" in sass and "SYNCS" in sass and "SHFL" in sass
     assert not re.search(r"\bBAR\.(SYNC|RED|ARV)", sass)
+
+
+@pytest.mark.parametrize("wl", [PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005),
+                                PI.small("local_laplacian", 256, 128), PI.small("camera", 96, 64),
+                                PI.small("harris", 64, 48)], ids=lambda w: w.pipeline)
+def test_inlining_preserves_the_definition(wl):
+    """The inlining pass (inline.cpp) rewrites the pipeline text; the oracle evaluates the rewritten text and
+    the text as written, and the liveouts must agree bit for bit (clamped substitution, stored-value casts)."""
+    import numpy as np
+    from oracle import evaluate
+    p = pmg.Pipeline(wl.text)
+    r = p.inlined(wl.params)
+    inp = wl.inputs("structured") if "laplacian" in wl.pipeline else wl.inputs()
+    a, b = evaluate(wl.text, wl.params, inp), evaluate(r["text"], wl.params, inp)
+    assert a.keys() == b.keys()
+    for k in a:
+        np.testing.assert_array_equal(a[k].view(np.uint8), b[k].view(np.uint8))
+    if "laplacian" in wl.pipeline:
+        assert "gP0" in r["inlined"] and "lP0" in r["inlined"]      # the 8-plane full-resolution stages
+    else:
+        assert r["inlined"] == []                                   # nothing data-expanding to substitute
