@@ -103,6 +103,10 @@ def cpu_baseline(wl, max_rows=None):
             "sample": f"{wl.name} {rows}x{W} full image x{reps} (numpy, single thread), {dt:.1f} s"}
 
 
+def metric_name(wl):
+    return f"output Mpixels/s ({wl.name}); % of HBM roofline"
+
+
 def reference_arm(args, wl):
     """--impl reference: the independent oracle timed on the host (no reference package exists)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -121,10 +125,10 @@ def reference_arm(args, wl):
     dt = (time.perf_counter() - t0) / args.steps
     v = W * rows / dt / 1e6
     print(json.dumps({
-        "impl": "reference", "metric": "output Mpixels/s (" + wl.name + ")", "value": v, "unit": "Mpixels/s",
+        "impl": "reference", "metric": metric_name(wl), "value": v, "unit": "Mpixels/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl.note, "sample_rows": rows},
+        "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "sample_rows": rows},
         "cpu_baseline": {"value": v, "unit": "Mpixels/s", "cores": 1, "kind": "oracle",
                          "sample": f"{rows} x {W} band per step (numpy, single thread)"},
         "e2e": {"value": v, "unit": "Mpixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
@@ -301,7 +305,7 @@ def main():
             dist.destroy_process_group()
         return
     line = {
-        "metric": f"output Mpixels/s ({wl.name}); % of HBM roofline", "value": value, "unit": "Mpixels/s",
+        "metric": metric_name(wl), "value": value, "unit": "Mpixels/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded U[0,1) image, pmg_inputs.py)",
