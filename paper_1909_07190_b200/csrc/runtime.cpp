@@ -256,6 +256,65 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   check(D.StreamCreate(&P->side, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
   check(D.EventCreate(&P->ev_fork, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
   check(D.EventCreate(&P->ev_join, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  // group DAG lanes: list-schedule the groups (topological order, weight = points of the group's domain) on up
+  // to 4 lanes; a group continues the lane of a producer when that lane is free at its ready time
+  {
+    const int ng = (int)P->sch.groups.size();
+    const Pipeline& pp = *P->pipe;
+    P->deps.assign(ng, {});
+    std::vector<int> gof(pp.stages.size(), -1);
+    for (int gi = 0; gi < ng; ++gi)
+      for (int s : P->sch.groups[gi].stages) gof[s] = gi;
+    for (int gi = 0; gi < ng; ++gi)
+      for (int s : P->sch.groups[gi].stages)
+        for (int q : pp.producers[s]) {
+          int gq = gof[q];
+          if (gq != gi && gq >= 0 && std::find(P->deps[gi].begin(), P->deps[gi].end(), gq) == P->deps[gi].end())
+            P->deps[gi].push_back(gq);
+        }
+    const int L = 4;
+    std::vector<double> lane_free(L, 0.0), fin(ng, 0.0);
+    P->lane_of.assign(ng, 0);
+    int used = 1;
+    for (int gi = 0; gi < ng; ++gi) {
+      const Group& g = P->sch.groups[gi];
+      double w = (double)g.npl * (double)g.ext.e[1] * (double)g.ext.e[2] + 1e4;   // + launch latency
+      double ready = 0;
+      for (int d : P->deps[gi]) ready = std::max(ready, fin[d]);
+      int best = 0;
+      double bs = 1e300;
+      for (int l = 0; l < L; ++l) {
+        double st = std::max(ready, lane_free[l]);
+        bool cont = false;
+        for (int d : P->deps[gi]) cont |= P->lane_of[d] == l;
+        st -= cont ? 1e-6 : 0;   // prefer continuing a producer's lane on ties
+        if (st < bs) { bs = st; best = l; }
+      }
+      P->lane_of[gi] = best;
+      fin[gi] = std::max(ready, lane_free[best]) + w;
+      lane_free[best] = fin[gi];
+      used = std::max(used, best + 1);
+    }
+    P->nlanes = used;
+    P->lane_stream.assign(used, nullptr);
+    P->lane_side.assign(used, nullptr);
+    P->lane_fork.assign(used, nullptr);
+    P->lane_join.assign(used, nullptr);
+    P->lane_side[0] = P->side;
+    P->lane_fork[0] = P->ev_fork;
+    P->lane_join[0] = P->ev_join;
+    for (int l = 1; l < used; ++l) {
+      check(D.StreamCreate(&P->lane_stream[l], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      check(D.StreamCreate(&P->lane_side[l], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      check(D.EventCreate(&P->lane_fork[l], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+      check(D.EventCreate(&P->lane_join[l], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    }
+    if (used > 1) {
+      P->ev_group.assign(ng, nullptr);
+      for (int gi = 0; gi < ng; ++gi) check(D.EventCreate(&P->ev_group[gi], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+      check(D.EventCreate(&P->ev_run, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    }
+  }
   return P;
 }
 
@@ -273,6 +332,12 @@ void plan_destroy(Plan* P) {
     for (CUevent e : P->ev_in) drv().EventDestroy(e);
     for (CUevent e : P->ev_done) drv().EventDestroy(e);
     if (P->ev_start) drv().EventDestroy(P->ev_start);
+    for (size_t l = 1; l < P->lane_stream.size(); ++l) drv().StreamDestroy(P->lane_stream[l]);
+    for (size_t l = 1; l < P->lane_side.size(); ++l) drv().StreamDestroy(P->lane_side[l]);
+    for (size_t l = 1; l < P->lane_fork.size(); ++l) drv().EventDestroy(P->lane_fork[l]);
+    for (size_t l = 1; l < P->lane_join.size(); ++l) drv().EventDestroy(P->lane_join[l]);
+    for (CUevent e : P->ev_group) drv().EventDestroy(e);
+    if (P->ev_run) drv().EventDestroy(P->ev_run);
     if (P->ev_end) drv().EventDestroy(P->ev_end);
     CUdevice dev;
     if (drv().DeviceGet(&dev, P->device) == CUDA_SUCCESS) drv().DevicePrimaryCtxRelease(dev);
@@ -383,9 +448,28 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
           throw Error(-3, "band mode: a liveout that is also consumed by the pipeline is not supported");
   }
   int64_t in_row_base = banded ? band_rows(P, band, nbands).in_r0 : 0;
+  const bool lanes = P.nlanes > 1;
+  std::vector<int> last_on_lane(P.nlanes, -1);
+  if (lanes) {
+    check(D.EventRecord(P.ev_run, s), "cuEventRecord");
+    for (int l = 1; l < P.nlanes; ++l) check(D.StreamWaitEvent(P.lane_stream[l], P.ev_run, 0), "cuStreamWaitEvent");
+  }
   for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) {
     const Group& g = P.sch.groups[gi];
     Kernel& K = P.kernels[gi];
+    const int lane = lanes ? P.lane_of[gi] : 0;
+    const CUstream gs = lane == 0 ? s : P.lane_stream[lane];
+    const CUstream gside = P.lane_side[lane];
+    const CUevent gfork = P.lane_fork[lane], gjoin = P.lane_join[lane];
+    if (lanes) {
+      for (int d : P.deps[gi])
+        if (P.lane_of[d] != lane) check(D.StreamWaitEvent(gs, P.ev_group[d], 0), "cuStreamWaitEvent");
+      last_on_lane[lane] = (int)gi;
+    }
+    struct Done {   // every group records its completion event, also when it launches nothing in this run
+      Drv& D; bool on; CUevent e; CUstream st;
+      ~Done() { if (on) D.EventRecord(e, st); }
+    } done{D, lanes, lanes ? P.ev_group[gi] : nullptr, gs};
     const int NT = std::max<int>(1, (int)g.tensors.size()), NTAB = std::max(1, P.ntables),
               NP = std::max<int>(1, (int)p.params.size());
     size_t off_tab = 40 * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
@@ -478,21 +562,23 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
       ++P.last_launches;
     };
     if (n_bdr > 0 && n_int > 0) {
-      // border tiles on the side stream, forked from and joined back into the caller's stream
-      check(D.EventRecord(P.ev_fork, s), "cuEventRecord");
-      check(D.StreamWaitEvent(P.side, P.ev_fork, 0), "cuStreamWaitEvent");
-      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, P.side, "_b");
-      launch(K.fn, K.blocks_per_sm, n_int, s, "");
-      check(D.EventRecord(P.ev_join, P.side), "cuEventRecord");
-      check(D.StreamWaitEvent(s, P.ev_join, 0), "cuStreamWaitEvent");
+      // border tiles on the lane's side stream, forked from and joined back into the lane's stream
+      check(D.EventRecord(gfork, gs), "cuEventRecord");
+      check(D.StreamWaitEvent(gside, gfork, 0), "cuStreamWaitEvent");
+      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
+      launch(K.fn, K.blocks_per_sm, n_int, gs, "");
+      check(D.EventRecord(gjoin, gside), "cuEventRecord");
+      check(D.StreamWaitEvent(gs, gjoin, 0), "cuStreamWaitEvent");
     } else if (n_int > 0) {
-      launch(K.fn, K.blocks_per_sm, n_int, s, "");
+      launch(K.fn, K.blocks_per_sm, n_int, gs, "");
     } else if (n_bdr > 0) {
-      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, s, "_b");
+      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gs, "_b");
     }
     (void)ntiles;
-
   }
+  if (lanes)   // join every lane back into the caller's stream
+    for (int l = 1; l < P.nlanes; ++l)
+      if (last_on_lane[l] >= 0) check(D.StreamWaitEvent(s, P.ev_group[last_on_lane[l]], 0), "cuStreamWaitEvent");
 }
 
 }  // namespace pmg

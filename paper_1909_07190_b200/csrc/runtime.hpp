@@ -54,6 +54,14 @@ struct Plan {
   CUevent ev_fork = nullptr, ev_join = nullptr;
   std::string json;
   std::vector<std::string> inlined;        // stages substituted into their readers (inline.cpp)
+  // independent groups run concurrently: each group is assigned a lane (lane 0 = the caller's stream,
+  // lanes 1.. plan-owned streams); cross-lane dependences are events (DESIGN.md §6 "group DAG")
+  int nlanes = 1;
+  std::vector<int> lane_of;                // per group
+  std::vector<std::vector<int>> deps;      // per group: the groups producing what it reads
+  std::vector<CUstream> lane_stream, lane_side;
+  std::vector<CUevent> lane_fork, lane_join, ev_group;
+  CUevent ev_run = nullptr;
   int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
   // host-buffer runs (pmg_run_host): copy streams and per-chunk events, created on first use
   CUstream h2d = nullptr, d2h = nullptr;
