@@ -101,74 +101,30 @@ struct Emitter {
     if (Uk % depth == 0) return ((u - b) % depth + depth) % depth;
     return b;
   }
-  // ---- register storage of rows ----
-  // Unpaired buffers: one scalar per element e in [-el, V+er).  Paired buffers (float rows, V even):
-  // float2 q_j = (e_j, e_{j+V/2}) for j in [-el, V/2+er), so that packed FADD2/FMUL2/FFMA2 results feed
-  // packed consumers without register moves; element e lives canonically in q_e.x (e < V/2, incl. the
-  // left extension) or q_{e-V/2}.y (e >= V/2, incl. the right extension); extension pairs also carry a
-  // copy of one core element ("pair completion").
-  bool pair_on() const { return V >= 2 && V % 2 == 0 && pair_stride() > 0; }
-  bool st_paired(int i) const { return pair_on() && p.stages[g.gs[i].id].dtype == DType::F32; }
-  bool sr_paired(int j) const { return pair_on() && g.streams[j].dtype == DType::F32; }
-  std::string qname(char pre, int i, int sl, int k, int j) const {
-    return std::string(1, pre) + std::to_string(i) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_q" + ename(j);
-  }
-  std::string canon(char pre, int i, int sl, int k, int e) const {
-    const int h = V / 2;
-    if (e < h) return qname(pre, i, sl, k, e) + ".x";
-    return qname(pre, i, sl, k, e - h) + ".y";
-  }
+  // ---- register storage of rows: one scalar per element e in [-el, V+er) of every window slot ----
   std::string sv(int i, int sl, int k, int e) const {
-    if (st_paired(i)) return canon('n', i, sl, k, e);
     return "n" + std::to_string(i) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_e" + ename(e);
   }
   std::string tv(int j, int sl, int k, int e) const {
-    if (sr_paired(j)) return canon('s', j, sl, k, e);
     return "s" + std::to_string(j) + "_r" + std::to_string(sl) + "_c" + std::to_string(k) + "_e" + ename(e);
   }
   // declare all slots of one buffer
-  void declare(char pre, int i, bool paired, bool isfloat, int depth, int el, int er) {
-    o << "    " << (paired ? "float2" : (isfloat ? "float" : "int")) << " ";
+  void declare(char pre, int i, bool isfloat, int depth, int el, int er) {
+    o << "    " << (isfloat ? "float" : "int") << " ";
     bool first = true;
     for (int sl = 0; sl < depth; ++sl)
-      for (int kk = 0; kk < TX; ++kk) {
-        if (paired) {
-          for (int j = -el; j < V / 2 + er; ++j) {
-            o << (first ? "" : ", ") << qname(pre, i, sl, kk, j) << " = make_float2(0.f, 0.f)";
-            first = false;
-          }
-        } else {
-          for (int e = -el; e < V + er; ++e) {
-            o << (first ? "" : ", ") << (pre == 'n' ? sv(i, sl, kk, e) : tv(i, sl, kk, e)) << " = 0";
-            first = false;
-          }
+      for (int kk = 0; kk < TX; ++kk)
+        for (int e = -el; e < V + er; ++e) {
+          o << (first ? "" : ", ") << (pre == 'n' ? sv(i, sl, kk, e) : tv(i, sl, kk, e)) << " = 0";
+          first = false;
         }
-      }
     o << ";\n";
   }
   // copy a whole row (all storage) from slot a to slot b
-  void copy_row(char pre, int i, bool paired, int el, int er, int a_, int b_, const std::string& ind) {
-    for (int kk = 0; kk < TX; ++kk) {
-      if (paired) {
-        for (int j = -el; j < V / 2 + er; ++j) o << ind << qname(pre, i, b_, kk, j) << " = " << qname(pre, i, a_, kk, j) << ";\n";
-      } else {
-        for (int e = -el; e < V + er; ++e)
-          o << ind << (pre == 'n' ? sv(i, b_, kk, e) : tv(i, b_, kk, e)) << " = " << (pre == 'n' ? sv(i, a_, kk, e) : tv(i, a_, kk, e)) << ";\n";
-      }
-    }
-  }
-  // fill the duplicated core element of every extension pair
-  void complete_pairs(char pre, int i, int sl, int el, int er, const std::string& ind) {
-    const int h = V / 2;
-    for (int kk = 0; kk < TX; ++kk) {
-      for (int j = -el; j < 0; ++j) {   // q_j = (e_j, e_{j+h}); e_{j+h} canonical elsewhere
-        std::string src = canon(pre, i, sl, kk, j + h);
-        o << ind << qname(pre, i, sl, kk, j) << ".y = " << src << ";\n";
-      }
-      for (int j = h; j < h + er; ++j) {  // q_j = (e_j, e_{j+h}): e_j is a core element
-        o << ind << qname(pre, i, sl, kk, j) << ".x = " << canon(pre, i, sl, kk, j) << ";\n";
-      }
-    }
+  void copy_row(char pre, int i, int el, int er, int a_, int b_, const std::string& ind) {
+    for (int kk = 0; kk < TX; ++kk)
+      for (int e = -el; e < V + er; ++e)
+        o << ind << (pre == 'n' ? sv(i, b_, kk, e) : tv(i, b_, kk, e)) << " = " << (pre == 'n' ? sv(i, a_, kk, e) : tv(i, a_, kk, e)) << ";\n";
   }
 
   // ---- expression emission (ctx: consumer stage pos i, chunk k, element v, sub-step u) ----
@@ -376,16 +332,6 @@ struct Emitter {
         int ri = site.at(&e);
         const GRead& gr = g.greads.at(g.read_map.at(ri));
         const GStage& C = g.gs[i];
-        if (vb == va + V / 2) {
-          if (gr.kind == RKind::STAGE && st_paired(gr.idx)) {
-            const GStage& P = g.gs[gr.idx];
-            return R2{true, qname('n', gr.idx, slot(depS(gr.idx), P.hi - C.hi - gr.dy - back_shift, u), k, va + gr.dx), {}, {}};
-          }
-          if (gr.kind == RKind::STREAM && sr_paired(gr.idx)) {
-            const GStream& S = g.streams[gr.idx];
-            return R2{true, qname('s', gr.idx, slot(depT(gr.idx), S.hi - C.hi - gr.dy - back_shift, u), k, va + gr.dx), {}, {}};
-          }
-        }
         R a = ex(e, Ctx{i, k, va, u}), b = ex(e, Ctx{i, k, vb, u});
         return R2{true, "make_float2(" + a.s + ", " + b.s + ")", {}, {}};
       }
@@ -475,7 +421,7 @@ struct Emitter {
     const int n = (int)g.gs.size();
     folds.assign(n, Fold{});
     const char* env = getenv("PMG_FOLD");
-    const bool enable = !(env && env[0] == '0') && !pair_on();
+    const bool enable = !(env && env[0] == '0');
     for (int i = 0; i < n && enable; ++i) {
       const StageDecl& sd = p.stages[g.gs[i].id];
       if (sd.dtype != DType::F32) continue;
@@ -566,7 +512,7 @@ struct Emitter {
     // opt-in (PMG_PACK=1): bit-exact, but on B200 the make_float2 MOVs cost what the packed FADD2s save
     // (harris 6400^2: 0.1198 ms packed vs 0.1169 ms scalar)
     const char* e = getenv("PMG_PACK");
-    return V >= 2 && V % 2 == 0 && e && (e[0] == '1' || e[0] == '2') && !pair_on();
+    return V >= 2 && V % 2 == 0 && e && (e[0] == '1' || e[0] == '2');
   }
   bool pack_stages() const { const char* e = getenv("PMG_PACK"); return pack_on() && e[0] == '1'; }   // '2': folds only
 
@@ -646,21 +592,11 @@ struct Emitter {
   // ---- kernel text ----
   int himax = 0, xlm = 0, xrm = 0;
 
-  // packed-pair stride: pairs (v, v + stride) inside a lane's V elements; 0 = scalar
-  int pair_stride() const {
-    if (V < 2 || V % 2) return 0;
-    const char* e = getenv("PMG_PAIR_STRIDE");   // experimental packed-pair storage (off by default)
-    int m = e ? atoi(e) : 0;
-    if (m <= 0) return 0;
-    return m == 1 ? 1 : V / 2;
-  }
-
   int phase_of(int t) const { return (((t - g.t_first) % Uk) + Uk) % Uk; }
 
   std::string run() {
     const KConfig& k = g.cfg;
     o << "// generated by libpmg (emit.cpp) for group " << g.name << ": ";
-    if (getenv("PMG_NO_PROXY_FENCE")) o << "\n#define PMG_NO_PROXY_FENCE 1\n// ";   // timing experiment only
     for (auto& s : g.gs) o << p.stages[s.id].name << " ";
     o << "\n#include \"pmg_otpw.cuh\"\n\n";
     for (auto& P : g.gs) himax = std::max(himax, P.hi);
@@ -815,11 +751,11 @@ struct Emitter {
     }
     for (int i = 0; i < n; ++i) {
       const GStage& P = g.gs[i];
-      declare('n', i, st_paired(i), p.stages[P.id].dtype == DType::F32, depS(i), P.el, P.er);
+      declare('n', i, p.stages[P.id].dtype == DType::F32, depS(i), P.el, P.er);
     }
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
-      declare('s', (int)j, sr_paired((int)j), S.dtype == DType::F32, depT((int)j), S.el, S.er);
+      declare('s', (int)j, S.dtype == DType::F32, depT((int)j), S.el, S.er);
     }
     for (int i = 0; i < n; ++i) {
       const Fold& f = folds[i];
@@ -894,8 +830,7 @@ struct Emitter {
 
   void shift_window(bool stage, int i, int depth, int el, int er, const std::string& ind) {
     // shift-mode window (depth does not divide the unroll factor): r{b} = r{b-1}
-    bool paired = stage ? st_paired(i) : sr_paired(i);
-    for (int b = depth - 1; b >= 1; --b) copy_row(stage ? 'n' : 's', i, paired, el, er, b - 1, b, ind);
+    for (int b = depth - 1; b >= 1; --b) copy_row(stage ? 'n' : 's', i, el, er, b - 1, b, ind);
   }
 
   void stream_reads(int u, bool fast, const std::string& ind) {
@@ -930,7 +865,6 @@ struct Emitter {
               << ", 0, W - 1) - xo);\n";
         o << ind << "  }\n";
       }
-      if (sr_paired((int)j)) complete_pairs('s', (int)j, sl, S.el, S.er, ind + "  ");
       o << ind << "}\n";
     }
     o << ind << "}\n" << ind << "__syncwarp();\n";
@@ -941,7 +875,7 @@ struct Emitter {
     std::string tt = tconst ? std::to_string(tval) : "t";
     if (rmode == 1) {
       // same tile, interior: rows need no clamp; the source pointers advance one row per step
-      if (g.streams.size() == 1 && !getenv("PMG_NO_ELECT")) {
+      if (g.streams.size() == 1) {
         o << ind << "{\n" << ind << "  pmg_refill1_elect(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, q_ptr0, p_bytes0);\n"
           << ind << "  q_ptr0 += a.t[" << g.streams[0].tensor_slot << "].row_pitch;\n" << ind << "}\n";
         return;
@@ -969,7 +903,7 @@ struct Emitter {
         << ind << "  const bool nx = s >= NSTEPS;\n"
         << ind << "  const int sr = nx ? s - NSTEPS : s;\n";
     }
-    if (g.streams.size() == 1 && !getenv("PMG_NO_ELECT")) {
+    if (g.streams.size() == 1) {
       const GStream& S = g.streams[0];
       o << ind << "  const int yq = nx ? pn_y0 : p_y0;\n"
         << ind << "  if (!nx || has_next)\n"
@@ -1108,13 +1042,7 @@ struct Emitter {
         o << in2 << "if (" << rowv << " >= 0 && " << rowv << " < H) {\n";
         in3 = in2 + "  ";
       }
-      if (st_paired(i) && pairable(*sd.expr)) {
-        for (int kk = 0; kk < TX; ++kk)
-          for (int v = 0; v < V / 2; ++v) {
-            R2 r = ex2(*sd.expr, i, kk, v, v + V / 2, u);
-            o << in3 << qname('n', i, cur, kk, v) << " = " << pack(r) << ";\n";
-          }
-      } else if (folded) {
+      if (folded) {
         // consumes the carried prefix first
         if (pack_on()) fold_segment_pair(i, (int)folds[i].m.size() - 1, u, cur, in3);
         else fold_segment(i, (int)folds[i].m.size() - 1, u, cur, in3);
@@ -1166,7 +1094,6 @@ struct Emitter {
           o << in3 << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + " << q << ") & 31);\n";
         }
       }
-      if (st_paired(i)) complete_pairs('n', i, cur, P.el, P.er, in3);
       if (hyb(i, 0)) {
         // hybrid tiling: the smem chunks' row goes to the window slot in shared memory; the first register
         // chunk also writes the head of its row into the right halo (reads across the S | S+1 boundary)
@@ -1186,9 +1113,9 @@ struct Emitter {
         if (PD > 1) {
           o << in3 << "if (" << rowv << " == 0) {\n";
           for (int sl = 0; sl < PD; ++sl)
-            if (sl != cur) copy_row('n', i, st_paired(i), P.el, P.er, cur, sl, in3 + "  ");
+            if (sl != cur) copy_row('n', i, P.el, P.er, cur, sl, in3 + "  ");
           o << in3 << "}\n" << in2 << "} else if (" << rowv << " >= H) {\n";
-          copy_row('n', i, st_paired(i), P.el, P.er, prev, cur, in3);
+          copy_row('n', i, P.el, P.er, prev, cur, in3);
         }
         o << in2 << "}\n";
       }

@@ -120,9 +120,7 @@ __device__ __forceinline__ void pmg_refill1_elect(u32 bar, u32 total, u32 dst, c
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
-#ifndef PMG_NO_PROXY_FENCE
       "@p fence.proxy.async.shared::cta;\n\t"
-#endif
       "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
       "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %4, [%0];\n}"
       ::"r"(bar), "r"(total), "r"(dst), "l"(src), "r"(bytes) : "memory");
