@@ -283,7 +283,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                  const pmg_sched_opts& o, CostBreakdown* out, const RegProbe* probe) {
   std::vector<int> Vs = o.vec > 0 ? std::vector<int>{o.vec} : std::vector<int>{1, 2, 4};
   std::vector<int> TXs = o.chunks > 0 ? std::vector<int>{o.chunks} : std::vector<int>{1, 2, 4};
-  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 64};
+  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 48, 64, 96};
   // NW: OTPW warps are independent, so the block size only sets the register budget ptxas plans for; one warp
   // per block was fastest or tied in every B200 sweep (profiles/sweep_r05_*), larger blocks via the override
   std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{1};
