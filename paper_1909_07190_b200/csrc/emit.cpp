@@ -77,6 +77,7 @@ struct Emitter {
   std::vector<int> dS, dT;
   int Uk = 1;
   bool in_interior = false;   // emitting the interior-tile kernel (hybrid smem chunks apply there only)
+  int cslot = -1;             // interior kernel: compile-time ring slot of the current step (-1: runtime)
 
   // hybrid tiling: stage i's window for chunk kk lives in warp-private shared memory (interior kernel,
   // chunks kk < S, rotating windows)
@@ -779,8 +780,17 @@ struct Emitter {
           o << "      const char* q_ptr" << j << " = p_src" << j << " + (i64)(p_y0 + (TFIRST + " << g.streams[j].hi
             << " + PREF)) * a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
       }
+      // compile-time ring slots when PREF divides the steps of a tile (every tile then starts at slot 0); the
+      // main loop is unrolled by lcm(U, PREF) so that every sub-step's slot is a constant
+      int L = Uk;
+      bool ct = hs && g.nsteps % k.PREF == 0;
+      if (ct) {
+        L = Uk / gcd_(Uk, k.PREF) * k.PREF;
+        if (L > 24) { ct = false; L = Uk; }
+      }
       for (int t = g.t_first; t < 0; ++t) {
         int s_ = t - g.t_first + k.PREF;
+        cslot = ct ? (t - g.t_first) % k.PREF : -1;
         step(true, phase_of(t), true, t, s_ < g.nsteps ? 1 : 0);
       }
       // running output row pointers of the main section and tail (row y0 + t + hi at step t = 0)
@@ -789,11 +799,12 @@ struct Emitter {
           o << "      char* optr" << i << " = obase" << i << " + (i64)(y0 + " << g.gs[i].hi << ") * a.t[" << g.gs[i].tensor_slot
             << "].row_pitch;\n";
       // main section: the refill of every step targets this tile (pointer increment, no clamp)
-      const int a_end = std::max(0, k.TH - k.PREF) / Uk * Uk;
+      const int a_end = std::max(0, k.TH - k.PREF) / L * L;
       if (a_end > 0) {
-        o << "      for (int tb = 0; tb < " << a_end << "; tb += " << Uk << ") {\n";
-        for (int u = 0; u < Uk; ++u) {
+        o << "      for (int tb = 0; tb < " << a_end << "; tb += " << L << ") {\n";
+        for (int u = 0; u < L; ++u) {
           o << "      { const int t = tb + " << u << ";\n";
+          cslot = ct ? ((u - g.t_first) % k.PREF + k.PREF) % k.PREF : -1;
           step(true, phase_of(u), false, 0, 1);
           o << "      }\n";
         }
@@ -801,14 +812,16 @@ struct Emitter {
       }
       if (a_end < k.TH) {
         // tail: the refills cross into the next tile (selects, clamped rows)
-        o << "      for (int tb = " << a_end << "; tb < TH; tb += " << Uk << ") {\n";
-        for (int u = 0; u < Uk; ++u) {
+        o << "      for (int tb = " << a_end << "; tb < TH; tb += " << L << ") {\n";
+        for (int u = 0; u < L; ++u) {
           o << "      { const int t = tb + " << u << ";\n      if (t < TH) {\n";
+          cslot = ct ? ((u - g.t_first) % k.PREF + k.PREF) % k.PREF : -1;
           step(true, phase_of(u), false, 0, 0);
           o << "      }\n      }\n";
         }
         o << "      }\n";
       }
+      cslot = -1;
       o << "    }\n";
     } else {
       // ---- border tiles: general bodies (clamped reads, edge replication, row checks) ----
@@ -834,10 +847,16 @@ struct Emitter {
   }
 
   void stream_reads(int u, bool fast, const std::string& ind) {
-    o << ind << "const int slq = c_slot;\n"
-      << ind << "pmg_mbar_wait(bar0 + 8 * slq, phase);\n"
-      << ind << "if (slq + 1 == PREF) { c_slot = 0; phase ^= 1u; } else { c_slot = slq + 1; }\n"
-      << ind << "{\n" << ind << "const char* srow = ring + slq * RING;\n";
+    if (cslot >= 0) {
+      // slot known at compile time (PREF divides the steps of a tile): constant addresses, one parity flip per lap
+      o << ind << "const int slq = " << cslot << ";\n" << ind << "pmg_mbar_wait(bar0 + 8 * slq, phase);\n";
+      if (cslot == g.cfg.PREF - 1) o << ind << "phase ^= 1u;\n";
+    } else {
+      o << ind << "const int slq = c_slot;\n"
+        << ind << "pmg_mbar_wait(bar0 + 8 * slq, phase);\n"
+        << ind << "if (slq + 1 == PREF) { c_slot = 0; phase ^= 1u; } else { c_slot = slq + 1; }\n";
+    }
+    o << ind << "{\n" << ind << "const char* srow = ring + slq * RING;\n";
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
       const int SD = depT((int)j);
