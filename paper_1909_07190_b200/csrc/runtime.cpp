@@ -540,21 +540,27 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
     int64_t txA = std::max<int64_t>(0, cdiv(g.PL + xlm, g.OW));
     int64_t txB = std::min<int64_t>(g.ntx, fdiv((int64_t)Wg - g.CW - xrm + g.PL, g.OW) + 1);
-    int64_t tyA = std::max<int64_t>(0, cdiv(-(int64_t)g.t_first - gy0, g.cfg.TH));
-    int64_t tyB = std::min<int64_t>({nty, fdiv((int64_t)Hg - g.cfg.TH - himax - gy0, g.cfg.TH) + 1,
-                                     fdiv((int64_t)gy1 - g.cfg.TH - gy0, g.cfg.TH) + 1});
-    if (txB <= txA || tyB <= tyA) txA = txB = tyA = tyB = 0;
-    const int64_t per = nty * g.ntx, n_int = (int64_t)nframes * g.npl * (tyB - tyA) * (txB - txA);
-    (void)per;
-    // border kernel: the same regions in TH_b-row tiles (TH_b divides TH)
-    const int THb = g.TH_b > 0 ? g.TH_b : g.cfg.TH, rb = g.cfg.TH / THb;
-    const int64_t nty_b = (gy1 - gy0 + THb - 1) / THb, tyA_b = tyA * rb, tyB_b = tyB * rb;
+    // interior tile rows: the tiling starts `top` rows below gy0 (a multiple of the border tile height, enough
+    // for the rows the wavefront reads above a tile), and holds the whole tiles whose wavefront stays inside
+    // the image and the computed rows; the border kernel takes the top and bottom remainders in TH_b-row tiles
+    // (TH_b divides TH), so at most TH_b - 1 + the halo rows of each image edge go through the general body
+    const int THb = g.TH_b > 0 ? g.TH_b : g.cfg.TH;
+    const int64_t top = cdiv(std::max<int64_t>(0, -(int64_t)g.t_first - gy0), THb) * THb;
+    const int64_t ylim = std::min<int64_t>((int64_t)Hg - himax, gy1);
+    int64_t nty_i = std::max<int64_t>(0, fdiv(ylim - gy0 - top, g.cfg.TH));
+    if (txB <= txA || nty_i <= 0) { txA = txB = 0; nty_i = 0; }
+    const int64_t gy0_i = gy0 + top;
+    const int64_t n_int = (int64_t)nframes * g.npl * nty_i * (txB - txA);
+    const int64_t nty_b = (gy1 - gy0 + THb - 1) / THb;
+    const int64_t tyA_b = nty_i > 0 ? top / THb : 0, tyB_b = nty_i > 0 ? tyA_b + nty_i * g.cfg.TH / THb : 0;
     const int64_t n_bdr = (int64_t)nframes * g.npl * (nty_b * g.ntx - (tyB_b - tyA_b) * (txB - txA));
+    (void)nty;
     void* args[] = {buf.data()};
     auto launch = [&](CUfunction f, int bps, int64_t nt, CUstream st, const char* what) {
       const bool bd = f == K.fn_b;
-      int32_t ints[14] = {Hg, Wg, gy0, gy1, (int32_t)(bd ? nty_b : nty), (int32_t)g.ntx, (int32_t)g.npl, (int32_t)nframes,
-                          (int32_t)nt, 0, (int32_t)txA, (int32_t)txB, (int32_t)(bd ? tyA_b : tyA), (int32_t)(bd ? tyB_b : tyB)};
+      int32_t ints[14] = {Hg, Wg, (int32_t)(bd ? gy0 : gy0_i), gy1, (int32_t)(bd ? nty_b : nty_i), (int32_t)g.ntx,
+                          (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0, (int32_t)txA, (int32_t)txB,
+                          (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : nty_i)};
       std::memcpy(buf.data() + off_int, ints, 56);
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
       CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);
