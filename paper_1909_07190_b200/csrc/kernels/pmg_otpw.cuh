@@ -101,6 +101,11 @@ union PmgVec {
 template <typename T, int N>
 __device__ __forceinline__ void pmg_stg_vec(char* dst, const T (&v)[N]) {
   constexpr int B = N * (int)sizeof(T);
+  if constexpr (B > 16 && B % 32 == 0) {  // V = 8 f32 lanes: two 16-byte stores
+    pmg_stg_vec<T, N / 2>(dst, reinterpret_cast<const T(&)[N / 2]>(v));
+    pmg_stg_vec<T, N / 2>(dst + B / 2, reinterpret_cast<const T(&)[N / 2]>(v[N / 2]));
+    return;
+  }
   PmgVec<T, N> u;
 #pragma unroll
   for (int i = 0; i < N; ++i) u.e[i] = v[i];
@@ -130,6 +135,11 @@ __device__ __forceinline__ void pmg_refill1_elect(u32 bar, u32 total, u32 dst, c
 template <typename T, int N>
 __device__ __forceinline__ void pmg_stg_vec_if(char* dst, const T (&v)[N], bool p) {
   constexpr int B = N * (int)sizeof(T);
+  if constexpr (B > 16 && B % 32 == 0) {
+    pmg_stg_vec_if<T, N / 2>(dst, reinterpret_cast<const T(&)[N / 2]>(v), p);
+    pmg_stg_vec_if<T, N / 2>(dst + B / 2, reinterpret_cast<const T(&)[N / 2]>(v[N / 2]), p);
+    return;
+  }
   PmgVec<T, N> u;
 #pragma unroll
   for (int i = 0; i < N; ++i) u.e[i] = v[i];
@@ -149,6 +159,11 @@ __device__ __forceinline__ void pmg_stg_vec_if(char* dst, const T (&v)[N], bool 
 template <typename T, int N>
 __device__ __forceinline__ void pmg_lds_vec(const char* src, T (&v)[N]) {
   constexpr int B = N * (int)sizeof(T);
+  if constexpr (B > 16 && B % 32 == 0) {
+    pmg_lds_vec<T, N / 2>(src, reinterpret_cast<T(&)[N / 2]>(v));
+    pmg_lds_vec<T, N / 2>(src + B / 2, reinterpret_cast<T(&)[N / 2]>(v[N / 2]));
+    return;
+  }
   PmgVec<T, N> u;
   if constexpr (B == 16) u.w16 = *reinterpret_cast<const uint4*>(src);
   else if constexpr (B == 8) u.w8 = *reinterpret_cast<const uint2*>(src);
