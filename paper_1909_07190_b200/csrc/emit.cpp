@@ -182,8 +182,50 @@ struct Emitter {
     return false;
   }
 
+  // x parity (the camera interleave, the pyramid upsampling): when every lane's first column xL is even
+  // (V, OW and PL even), `x + b` has a known parity per element, so `(x + b) % 2` is a constant and
+  // `(x + b) / 2` (floor) is xL/2 plus a constant -- exact integer identities, no change of results
+  bool x_even() const { return V % 2 == 0 && g.OW % 2 == 0 && g.PL % 2 == 0; }
+  bool affine_x(const Expr& e, const Ctx& c, int64_t* off) {
+    if (e.op == Expr::VAR) {
+      int nd = (int)p.stages[g.gs[c.i].id].vars.size();
+      if (e.index + 3 - nd != 2) return false;
+      *off = 32 * V * c.k + c.v;
+      return true;
+    }
+    if (e.op == Expr::BIN && e.kind == Kind::Int && (e.text == "+" || e.text == "-")) {
+      int64_t o;
+      if (e.args[1]->op == Expr::INT && affine_x(*e.args[0], c, &o)) {
+        *off = e.text == "+" ? o + e.args[1]->ival : o - e.args[1]->ival;
+        return true;
+      }
+      if (e.text == "+" && e.args[0]->op == Expr::INT && affine_x(*e.args[1], c, &o)) {
+        *off = o + e.args[0]->ival;
+        return true;
+      }
+    }
+    return false;
+  }
+
   R bin(const Expr& e, const Ctx& c) {
     const std::string& op = e.text;
+    int64_t xo;
+    if ((op == "%" || op == "/") && e.kind == Kind::Int && e.args[1]->op == Expr::INT && e.args[1]->ival == 2 && x_even() &&
+        affine_x(*e.args[0], c, &xo)) {
+      int64_t fl = xo >= 0 ? xo / 2 : -((-xo + 1) / 2);   // floor(xo / 2)
+      if (op == "%") return {"(" + std::to_string(xo - 2 * fl) + ")", Kind::Int};
+      return {"(xLh + " + std::to_string(fl) + ")", Kind::Int};
+    }
+    // floor division and non-negative remainder by a power of two are an arithmetic shift and a mask
+    // (two's complement int32, reading R4): exact for every sign
+    if ((op == "%" || op == "/") && e.kind == Kind::Int && e.args[1]->op == Expr::INT && e.args[1]->ival >= 2 &&
+        e.args[1]->ival <= (1 << 30) && (e.args[1]->ival & (e.args[1]->ival - 1)) == 0) {
+      R a = ex(*e.args[0], c);
+      int k = 0;
+      while ((int64_t(1) << k) < e.args[1]->ival) ++k;
+      if (op == "%") return {"((" + a.s + ") & " + std::to_string(e.args[1]->ival - 1) + ")", Kind::Int};
+      return {"((" + a.s + ") >> " + std::to_string(k) + ")", Kind::Int};
+    }
     if (op == "&&" || op == "||") {
       R a = ex(*e.args[0], c), b = ex(*e.args[1], c);
       return {"(((" + a.s + ") != 0) " + op + " ((" + b.s + ") != 0) ? 1 : 0)", Kind::Int};
@@ -733,9 +775,10 @@ struct Emitter {
          "    const int y0 = a.gy0 + ty * TH;\n"
          "    const int cx = tx * OW - PL;\n"
          "    const int xL = cx + V * lane;\n"
+         "    const int xLh = xL >> 1;   // xL / 2 (used only when xL is even)\n"
          "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W);\n"
          "    const int yend = (y0 + TH < a.gy1) ? (y0 + TH) : a.gy1;\n"
-         "    (void)pc; (void)fr; (void)xL; (void)xb; (void)yend;\n";
+         "    (void)pc; (void)fr; (void)xL; (void)xLh; (void)xb; (void)yend;\n";
     if (hs) {
       o << "    const bool has_next = it + 1 < my_tiles;\n"
            "    if (has_next) p_params(tile + nwt, pn_y0, pn_total";

@@ -33,9 +33,17 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   for (int s : p.topo)
     if (gos[s] == gid) order.push_back(s);
   g.stages = order;
+  // a group iterates one (plane, y, x) domain; stages without a plane dim may join a plane group when their
+  // (y, x) extents match ("broadcast" stages: recomputed for every plane, never materialised -- checked below)
   g.ext = A.stage_ext[order[0]];
   for (int s : order)
-    if (!(A.stage_ext[s] == g.ext)) return bad("stages of different extents (" + p.stages[s].name + ")");
+    if (A.stage_ext[s].has[0]) g.ext = A.stage_ext[s];
+  for (int s : order) {
+    const Ext3& e = A.stage_ext[s];
+    if (e == g.ext) continue;
+    if (e.has[0] || !g.ext.has[0] || e.e[1] != g.ext.e[1] || e.e[2] != g.ext.e[2] || e.has[1] != g.ext.has[1])
+      return bad("stages of different extents (" + p.stages[s].name + ")");
+  }
   const int n = (int)order.size();
   std::vector<int> pos(p.stages.size(), -1);
   for (int i = 0; i < n; ++i) pos[order[i]] = i;
@@ -47,6 +55,7 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
     for (int c : p.consumers[s])
       if (gos[c] != gid) lo = true;
     g.gs[i].materialize = lo;
+    if (lo && !(A.stage_ext[s] == g.ext)) return bad("broadcast stage " + p.stages[s].name + " must be materialised");
   }
   // resolve reads
   g.read_map.assign(A.reads.size(), -1);

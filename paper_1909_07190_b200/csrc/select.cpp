@@ -274,8 +274,17 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
 
 static bool feasible_stage_set(const Analysis& A, const std::vector<int>& stages) {
   // cheap pre-check: same extents
-  for (int s : stages)
-    if (!(A.stage_ext[s] == A.stage_ext[stages[0]])) return false;
+  // same (y, x) extents; plane dims equal or absent (broadcast stages in a plane group, group.cpp)
+  const Ext3* pe = nullptr;
+  for (int s : stages) {
+    const Ext3& e = A.stage_ext[s];
+    const Ext3& f = A.stage_ext[stages[0]];
+    if (e.e[1] != f.e[1] || e.e[2] != f.e[2] || e.has[1] != f.has[1]) return false;
+    if (e.has[0]) {
+      if (pe && !(*pe == e)) return false;
+      pe = &e;
+    }
+  }
   return true;
 }
 

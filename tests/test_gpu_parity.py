@@ -90,6 +90,28 @@ def test_camera_parity():
     check("camera", 264, 130)
 
 
+PARITY_SWEEP = [dict(vec=v, chunks=tx, rows=th, warps=1, prefetch=pf)
+                for (v, tx, th, pf) in [(1, 1, 3, 2), (2, 1, 8, 4), (2, 2, 5, 3), (4, 1, 16, 4), (4, 2, 8, 2)]]
+
+
+@pytest.mark.parametrize("cfg", PARITY_SWEEP, ids=lambda c: "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
+@pytest.mark.parametrize("W,H", [(264, 130), (263, 131)])
+def test_camera_schedules(cfg, W, H):
+    """x-parity folding of `x % 2` / `x / 2` (even V) and the shift/mask forms of floor division: the camera
+    pipe's interleave and deinterleave under every lane width, on even and odd extents."""
+    check("camera", W, H, opts=pmg.sched_opts(**cfg, tx_size=32))
+
+
+@pytest.mark.parametrize("cfg", PARITY_SWEEP[:3], ids=lambda c: "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
+def test_local_laplacian_schedules(cfg):
+    w = PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 97, "H": 63}, 1005)
+    inp = w.inputs("structured")
+    exp = evaluate(w.text, w.params, inp)
+    got, _ = run_gpu(w.text, w.params, inp, opts=pmg.sched_opts(**cfg, tx_size=32))
+    neq, _ = compare(got["out"], exp["out"], float_tol=1e-4)
+    assert neq == 0
+
+
 def test_local_laplacian_small_parity():
     w = PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005)
     inp = w.inputs("structured")

@@ -53,7 +53,12 @@ def main():
     nbytes = None
     for spec in ["auto"] + specs:
         try:
-            opts = None if spec == "auto" else pmg.sched_opts(**{k: int(v) for k, v in (x.split("=") for x in spec.split(","))})
+            # gos=0.1.1.2 gives group_of_stage (one group id per stage, '.'-separated)
+            kv = {k: ([int(q) for q in v.split(".")] if k == "gos" else int(v))
+                  for k, v in (x.split("=") for x in spec.split(","))} if spec != "auto" else None
+            if kv and "gos" in kv:
+                kv["group_of_stage"] = kv.pop("gos")
+            opts = None if spec == "auto" else pmg.sched_opts(**kv)
             plan = pmg.Plan(pipe, wl.params, opts=opts)
             if nbytes is None:
                 nbytes = sum(int(torch.tensor(io.shape).prod()) * pmg._binding.DTYPE_SIZE[io.dtype]
