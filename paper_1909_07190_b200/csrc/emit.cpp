@@ -77,6 +77,7 @@ struct Emitter {
   std::vector<int> dS, dT;
   int Uk = 1;
   bool in_interior = false;   // emitting the interior-tile kernel (hybrid smem chunks apply there only)
+  bool xk = false;            // emitting the x-border kernel: interior bodies + clamped columns, edge fix-up, bounded stores
   int cslot = -1;             // interior kernel: compile-time ring slot of the current step (-1: runtime)
 
   // hybrid tiling: stage i's window for chunk kk lives in warp-private shared memory (interior kernel,
@@ -330,7 +331,8 @@ struct Emitter {
       const GStream& S = g.streams[gr.idx];
       int b = S.hi - C.hi - gr.dy;
       b -= back_shift;
-      return {tv(gr.idx, slot(depT(gr.idx), b, c.u), c.k, c.v + gr.dx), dtype_is_float(S.dtype) ? Kind::Float : Kind::Int};
+      const int e = (S.sx == 1 ? 2 * c.v : c.v) + gr.dx;   // register index (down2: q = 2e + b)
+      return {tv(gr.idx, slot(depT(gr.idx), b, c.u), c.k, e), dtype_is_float(S.dtype) ? Kind::Float : Kind::Int};
     }
     // gather: per-element global load with clamped indices (any index form)
     const ReadSite& r = A.reads[ri];
@@ -644,7 +646,8 @@ struct Emitter {
     o << "\n#include \"pmg_otpw.cuh\"\n\n";
     for (auto& P : g.gs) himax = std::max(himax, P.hi);
     for (auto& S : g.streams) himax = std::max(himax, S.hi);
-    for (auto& S : g.streams) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
+    for (auto& S : g.streams)
+      if (S.sx == 0) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
     o << "#define V " << V << "\n#define TX " << TX << "\n#define CW " << g.CW << "\n#define PL " << g.PL
       << "\n#define OW " << g.OW << "\n#define TH " << k.TH << "\n#define NW " << k.NW << "\n#define PREF " << k.PREF
       << "\n#define TFIRST " << g.t_first << "\n#define NSTEPS " << g.nsteps << "\n#define USTEP " << g.U
@@ -671,7 +674,24 @@ struct Emitter {
          "  if (kk < bot) { ty = a.tyB + kk / a.ntx; tx = kk % a.ntx; return; }\n"
          "  kk -= bot;\n"
          "  const int side = a.ntx - (a.txB - a.txA);\n"
-         "  ty = a.tyA + kk / side; const int j = kk % side; tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
+         "  ty = a.tyA + kk / side; const int j = kk % side; tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n"
+         "__device__ __forceinline__ void pmg_tile_x(const PmgArgs& a, int t, int& tx, int& ty, int& pc, int& fr) {\n"
+         "  const int side = a.ntx - (a.txB - a.txA), h = a.tyB - a.tyA;\n"
+         "  const int j = t % side; int r = t / side; ty = a.tyA + r % h; r /= h; pc = r % a.npl; fr = r / a.npl;\n"
+         "  tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
+    kernel(true);
+    return o.str();
+  }
+
+  // the x-border kernel: tiles of the first / last tile columns whose rows are interior, with TH_x-row
+  // tiles, run the interior (branch-free in y) bodies with clamped columns, edge replication and bounded stores
+  std::string run_xborder() {
+    for (auto& P : g.gs) himax = std::max(himax, P.hi);
+    for (auto& S : g.streams) himax = std::max(himax, S.hi);
+    for (auto& S : g.streams)
+      if (S.sx == 0) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
+    o << "#undef TH\n#undef NSTEPS\n#define TH " << g.cfg.TH << "\n#define NSTEPS " << g.nsteps << "\n\n";
+    xk = true;
     kernel(true);
     return o.str();
   }
@@ -680,7 +700,8 @@ struct Emitter {
   std::string run_border() {
     for (auto& P : g.gs) himax = std::max(himax, P.hi);
     for (auto& S : g.streams) himax = std::max(himax, S.hi);
-    for (auto& S : g.streams) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
+    for (auto& S : g.streams)
+      if (S.sx == 0) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
     o << "#undef TH\n#undef NSTEPS\n#define TH " << g.cfg.TH << "\n#define NSTEPS " << g.nsteps << "\n\n";
     kernel(false);
     return o.str();
@@ -697,8 +718,8 @@ struct Emitter {
       folds.assign(n, Fold{});
       Uk = g.U;
     }
-    in_interior = interior;
-    const char* dec = interior ? "pmg_tile_int" : "pmg_tile_bdr";
+    in_interior = interior && !xk;
+    const char* dec = xk ? "pmg_tile_x" : interior ? "pmg_tile_int" : "pmg_tile_bdr";
     int cap = k.regcap;
     if (!interior && cap <= 0) {
       // border tiles are latency-bound and share the SMs with the interior kernel: cap their registers so
@@ -709,7 +730,7 @@ struct Emitter {
       cap = e ? atoi(e) : (g.regs_est > 0 && g.regs_est <= 72 ? 96 : 0);
     }
     int minb = cap > 0 ? std::max(1, 65536 / (cap * 32 * k.NW)) : 1;
-    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << (interior ? "" : "_b")
+    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << (xk ? "_x" : interior ? "" : "_b")
       << "(const __grid_constant__ PmgArgs a) {\n";
     o << "  extern __shared__ __align__(128) char pmg_smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
@@ -748,8 +769,8 @@ struct Emitter {
         int Aal = 16 / S.esz;
         o << "    {\n      const PmgTensor& T = a.t[" << S.tensor_slot << "];\n"
           << "      const int pl = " << (S.plane_mode == 0 ? "0" : S.plane_mode == 1 ? "pcq" : std::to_string(S.plane_const)) << ";\n"
-          << "      const int xlo = cxq - " << S.xl << ", xhi = cxq + CW + " << S.xr << ";\n"
-          << "      const int wa = (W + " << (Aal - 1) << ") / " << Aal << " * " << Aal << ";\n"
+          << "      const int xlo = " << pcol(S, "cxq") << " - " << S.xl << ", xhi = xlo + " << S.row_elems << ";\n"
+          << "      const int wa = (" << (S.sx == 0 ? std::string("W") : "T.W") << " + " << (Aal - 1) << ") / " << Aal << " * " << Aal << ";\n"
           << "      const int clo = xlo < 0 ? 0 : xlo, chi = xhi > wa ? wa : xhi;\n"
           << "      src" << j << " = T.ptr + (i64)frq * T.frame_stride + (i64)pl * T.plane_pitch - (i64)T.row_base * T.row_pitch + (i64)clo * " << S.esz << ";\n"
           << "      dst" << j << " = " << S.smem_off << " + (u32)(clo - xlo) * " << S.esz << ";\n"
@@ -765,8 +786,9 @@ struct Emitter {
            "    const u32 bar = bar0 + 8 * s;\n"
            "    pmg_mbar_expect_tx_if(bar, p_total, leader);\n";
       for (size_t j = 0; j < g.streams.size(); ++j)
-        o << "    pmg_bulk_g2s_if(ring_addr + s * RING + p_dst" << j << ", p_src" << j << " + (i64)pmg_clampi(p_y0 + (TFIRST + "
-          << g.streams[j].hi << ") + s, 0, H - 1) * a.t[" << g.streams[j].tensor_slot << "].row_pitch, p_bytes" << j << ", bar, leader);\n";
+        o << "    pmg_bulk_g2s_if(ring_addr + s * RING + p_dst" << j << ", p_src" << j << " + (i64)"
+          << prow((int)j, "p_y0 + (TFIRST + " + std::to_string(g.streams[j].hi) + ") + s") << " * a.t[" << g.streams[j].tensor_slot
+          << "].row_pitch, p_bytes" << j << ", bar, leader);\n";
       o << "  }\n  int c_slot = 0;\n  u32 phase = 0u;   // parity of the ring's current lap (all slots are used round-robin)\n";
     }
     o << "  for (int it = 0; it < my_tiles; ++it) {\n"
@@ -776,7 +798,7 @@ struct Emitter {
          "    const int cx = tx * OW - PL;\n"
          "    const int xL = cx + V * lane;\n"
          "    const int xLh = xL >> 1;   // xL / 2 (used only when xL is even)\n"
-         "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W);\n"
+         "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W)" << xb_scaled() << ";\n"
          "    const int yend = (y0 + TH < a.gy1) ? (y0 + TH) : a.gy1;\n"
          "    (void)pc; (void)fr; (void)xL; (void)xLh; (void)xb; (void)yend;\n";
     if (hs) {
@@ -820,8 +842,9 @@ struct Emitter {
       o << "    {\n";
       if (hs) {
         for (size_t j = 0; j < g.streams.size(); ++j)
-          o << "      const char* q_ptr" << j << " = p_src" << j << " + (i64)(p_y0 + (TFIRST + " << g.streams[j].hi
-            << " + PREF)) * a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
+          if (g.streams[j].sy == 0)
+            o << "      const char* q_ptr" << j << " = p_src" << j << " + (i64)(p_y0 + (TFIRST + " << g.streams[j].hi
+              << " + PREF)) * a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
       }
       // compile-time ring slots when PREF divides the steps of a tile (every tile then starts at slot 0); the
       // main loop is unrolled by lcm(U, PREF) so that every sub-step's slot is a constant
@@ -889,6 +912,32 @@ struct Emitter {
     for (int b = depth - 1; b >= 1; --b) copy_row(stage ? 'n' : 's', i, el, er, b - 1, b, ind);
   }
 
+  // x-border condition of the scaled streams: the tile's smem row would leave [0, Wp) of the producer
+  std::string xb_scaled() const {
+    std::string r;
+    for (const auto& S : g.streams) {
+      if (S.sx == 0) continue;
+      std::string o0 = "(" + pcol(S, "cx") + " - " + std::to_string(S.xl) + ")";
+      r += " || " + o0 + " < 0 || " + o0 + " + " + std::to_string(S.row_elems) + " > a.t[" + std::to_string(S.tensor_slot) + "].W";
+    }
+    return r;
+  }
+
+  // producer row of stream j at virtual row R (clamped to the producer's rows, reading R1)
+  std::string prow(int j, const std::string& R) const {
+    const GStream& S = g.streams[j];
+    std::string Hp = "a.t[" + std::to_string(S.tensor_slot) + "].H - 1";
+    if (S.sy == 1) return "pmg_clampi(2 * (" + R + ") + " + std::to_string(S.py) + ", 0, " + Hp + ")";
+    if (S.sy == 2) return "pmg_clampi((" + R + ") >> 1, 0, " + Hp + ")";
+    return "pmg_clampi(" + R + ", 0, H - 1)";
+  }
+  // producer column of consumer column `c` (the chunk origin) for the x form of stream j
+  static std::string pcol(const GStream& S, const std::string& c) {
+    if (S.sx == 1) return "(2 * (" + c + "))";
+    if (S.sx == 2) return "((" + c + ") >> 1)";
+    return "(" + c + ")";
+  }
+
   void stream_reads(int u, bool fast, const std::string& ind) {
     if (cslot >= 0) {
       // slot known at compile time (PREF divides the steps of a tile): constant addresses, one parity flip per lap
@@ -911,20 +960,43 @@ struct Emitter {
       int vlo = (int)std::floor((double)lo / V) * V, vhi = (int)std::ceil((double)hi / V) * V;
       o << ind << "{\n" << ind << "  const char* sb = srow + " << S.smem_off << ";\n";
       if (!fast) o << ind << "  if (!xb) {\n";
-      for (int kk = 0; kk < TX; ++kk)
-        for (int vb = vlo; vb < vhi; vb += V) {
-          o << ind << "    { " << ct << " w[" << V << "]; pmg_lds_vec<" << ct << ", " << V << ">(sb + (" << S.xl << " + "
-            << 32 * V * kk << " + V * lane + (" << vb << ")) * " << S.esz << ", w);";
-          for (int q = 0; q < V; ++q)
-            if (vb + q >= lo && vb + q < hi) o << " " << tv((int)j, sl, kk, vb + q) << " = PmgElem<" << ct << ">::cv(w[" << q << "]);";
-          o << " }\n";
-        }
-      if (!fast) {
-        o << ind << "  } else {\n" << ind << "    const int xo = cx - " << S.xl << ";\n";
+      if (fast && xk) o << ind << "  if (false) {\n";   // x-border kernel: every tile is an x-border tile
+      if (S.sx == 2) {
+        // up2: lane base (V/2)*lane; e' -> element floor(e'/2); vectors of V/2 elements
+        const int h = V / 2, qlo = (int)std::floor(lo / 2.0), qhi = (hi - 1) / 2;
         for (int kk = 0; kk < TX; ++kk)
-          for (int e = lo; e < hi; ++e)
-            o << ind << "    " << tv((int)j, sl, kk, e) << " = pmg_lds<" << ct << ">(sb, pmg_clampi(xL + " << 32 * V * kk + e
-              << ", 0, W - 1) - xo);\n";
+          for (int qb = (int)std::floor((double)qlo / h) * h; qb <= qhi; qb += h) {
+            o << ind << "    { " << ct << " w[" << h << "]; pmg_lds_vec<" << ct << ", " << h << ">(sb + (" << S.xl << " + "
+              << 16 * V * kk << " + " << h << " * lane + (" << qb << ")) * " << S.esz << ", w);";
+            for (int e = lo; e < hi; ++e) {
+              int q = (int)std::floor(e / 2.0);
+              if (q >= qb && q < qb + h) o << " " << tv((int)j, sl, kk, e) << " = PmgElem<" << ct << ">::cv(w[" << q - qb << "]);";
+            }
+            o << " }\n";
+          }
+      } else {
+        const int lb = S.sx == 1 ? 2 * V : V;   // lane stride in producer elements
+        for (int kk = 0; kk < TX; ++kk)
+          for (int vb = vlo; vb < vhi; vb += V) {
+            o << ind << "    { " << ct << " w[" << V << "]; pmg_lds_vec<" << ct << ", " << V << ">(sb + (" << S.xl << " + "
+              << 32 * lb * kk << " + " << lb << " * lane + (" << vb << ")) * " << S.esz << ", w);";
+            for (int q = 0; q < V; ++q)
+              if (vb + q >= lo && vb + q < hi) o << " " << tv((int)j, sl, kk, vb + q) << " = PmgElem<" << ct << ">::cv(w[" << q << "]);";
+            o << " }\n";
+          }
+      }
+      if (!fast || xk) {
+        // clamped producer columns (reading R1): unit xL+e, down2 2*xL+q, up2 floor((xL+e')/2)
+        const std::string Wp = S.sx == 0 ? "W - 1" : "a.t[" + std::to_string(S.tensor_slot) + "].W - 1";
+        o << ind << "  } else {\n" << ind << "    const int xo = " << pcol(S, "cx") << " - " << S.xl << ";\n";
+        for (int kk = 0; kk < TX; ++kk)
+          for (int e = lo; e < hi; ++e) {
+            std::string col = S.sx == 1 ? "2 * (xL + " + std::to_string(32 * V * kk) + ") + (" + std::to_string(e) + ")"
+                              : S.sx == 2 ? "(xL + " + std::to_string(32 * V * kk + e) + ") >> 1"
+                                          : "xL + " + std::to_string(32 * V * kk + e);
+            o << ind << "    " << tv((int)j, sl, kk, e) << " = pmg_lds<" << ct << ">(sb, pmg_clampi(" << col << ", 0, " << Wp
+              << ") - xo);\n";
+          }
         o << ind << "  }\n";
       }
       o << ind << "}\n";
@@ -936,10 +1008,20 @@ struct Emitter {
   void refill(bool tconst, int tval, int rmode, const std::string& ind) {
     std::string tt = tconst ? std::to_string(tval) : "t";
     if (rmode == 1) {
-      // same tile, interior: rows need no clamp; the source pointers advance one row per step
+      // same tile, interior: rows need no clamp; the source pointers advance one row per step (scaled rows:
+      // the clamped producer row of the virtual row requested, p_y0 + hi + t + PREF)
+      auto src_of = [&](int j) {
+        if (g.streams[j].sy == 0) return "q_ptr" + std::to_string(j);
+        return "p_src" + std::to_string(j) + " + (i64)" + prow(j, "p_y0 + " + std::to_string(g.streams[j].hi) + " + " + tt + " + PREF") +
+               " * a.t[" + std::to_string(g.streams[j].tensor_slot) + "].row_pitch";
+      };
+      auto adv = [&](int j) {
+        return g.streams[j].sy == 0 ? "  q_ptr" + std::to_string(j) + " += a.t[" + std::to_string(g.streams[j].tensor_slot) + "].row_pitch;\n"
+                                    : std::string();
+      };
       if (g.streams.size() == 1) {
-        o << ind << "{\n" << ind << "  pmg_refill1_elect(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, q_ptr0, p_bytes0);\n"
-          << ind << "  q_ptr0 += a.t[" << g.streams[0].tensor_slot << "].row_pitch;\n" << ind << "}\n";
+        o << ind << "{\n" << ind << "  pmg_refill1_elect(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, " << src_of(0)
+          << ", p_bytes0);\n" << ind << adv(0) << ind << "}\n";
         return;
       }
       o << ind << "{\n" << ind << "  const u32 bar = bar0 + 8 * slq;\n"
@@ -947,10 +1029,9 @@ struct Emitter {
         << ind << "    pmg_fence_proxy_async();\n"
         << ind << "    pmg_mbar_expect_tx(bar, p_total);\n";
       for (size_t j = 0; j < g.streams.size(); ++j)
-        o << ind << "    pmg_bulk_g2s(ring_addr + slq * RING + p_dst" << j << ", q_ptr" << j << ", p_bytes" << j << ", bar);\n";
+        o << ind << "    pmg_bulk_g2s(ring_addr + slq * RING + p_dst" << j << ", " << src_of((int)j) << ", p_bytes" << j << ", bar);\n";
       o << ind << "  }\n";
-      for (size_t j = 0; j < g.streams.size(); ++j)
-        o << ind << "  q_ptr" << j << " += a.t[" << g.streams[j].tensor_slot << "].row_pitch;\n";
+      for (size_t j = 0; j < g.streams.size(); ++j) o << ind << adv((int)j);
       o << ind << "}\n";
       return;
     }
@@ -970,7 +1051,7 @@ struct Emitter {
       o << ind << "  const int yq = nx ? pn_y0 : p_y0;\n"
         << ind << "  if (!nx || has_next)\n"
         << ind << "    pmg_refill1_elect(bar0 + 8 * slq, nx ? pn_total : p_total, ring_addr + slq * RING + (nx ? pn_dst0 : p_dst0), "
-        << "(nx ? pn_src0 : p_src0) + (i64)pmg_clampi(yq + (TFIRST + " << S.hi << ") + sr, 0, H - 1) * a.t[" << S.tensor_slot
+        << "(nx ? pn_src0 : p_src0) + (i64)" << prow(0, "yq + (TFIRST + " + std::to_string(S.hi) + ") + sr") << " * a.t[" << S.tensor_slot
         << "].row_pitch, nx ? pn_bytes0 : p_bytes0);\n" << ind << "}\n";
       return;
     }
@@ -982,7 +1063,7 @@ struct Emitter {
     for (size_t j = 0; j < g.streams.size(); ++j) {
       const GStream& S = g.streams[j];
       o << ind << "  pmg_bulk_g2s_if(ring_addr + slq * RING + (nx ? pn_dst" << j << " : p_dst" << j << "), (nx ? pn_src" << j
-        << " : p_src" << j << ") + (i64)pmg_clampi(yq + (TFIRST + " << S.hi << ") + sr, 0, H - 1) * a.t[" << S.tensor_slot
+        << " : p_src" << j << ") + (i64)" << prow((int)j, "yq + (TFIRST + " + std::to_string(S.hi) + ") + sr") << " * a.t[" << S.tensor_slot
         << "].row_pitch, nx ? pn_bytes" << j << " : p_bytes" << j << ", bar, go);\n";
     }
     o << ind << "}\n";
@@ -1007,6 +1088,12 @@ struct Emitter {
       if (check_rows) pred = "(" + rowv + " < yend) && " + pred;
       o << ind << "{\n" << ind << "  char* orow = optr" << i << ";\n" << ind << "  optr" << i << " += " << T << ".row_pitch;\n"
         << ind << "  const bool sp = " << pred << ";\n";
+      if (xk) {
+        o << ind << "  if (sp) {\n";
+        bounded_store(i, cur, "orow", ind + "    ");
+        o << ind << "  }\n" << ind << "}\n";
+        return;
+      }
       for (int kk = 0; kk < TX; ++kk) {
         int lo = g.PL - 32 * V * kk <= 0 ? 0 : std::min(32, (g.PL - 32 * V * kk) / V);
         int hi = std::max(0, std::min(32, (g.CW - g.PR - 32 * V * kk) / V));
@@ -1025,6 +1112,11 @@ struct Emitter {
     if (check_rows) o << ind << "if (" << rowv << " >= y0 && " << rowv << " < yend && " << inbuf << ") {\n";
     else o << ind << "if (" << inbuf << ") {\n";
     o << ind << "  char* orow = obase" << i << " + (i64)" << rowv << " * a.t[" << P.tensor_slot << "].row_pitch;\n";
+    if (fast && xk) {
+      bounded_store(i, cur, "orow", ind + "  ");
+      o << ind << "}\n" << ind << "}\n";
+      return;
+    }
     if (!fast)
       o << ind << "  const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
         << ind << "  const int oxhi = (cx + PL + OW) < W ? (cx + PL + OW) : W;\n";
@@ -1055,6 +1147,30 @@ struct Emitter {
     }
     o << ind << "}\n";
     o << ind << "}\n";
+  }
+
+  // store of one row of stage i at `orow` limited to the tile's output columns inside [0, W) (x-border
+  // kernel; partial vectors at the image edge)
+  void bounded_store(int i, int cur, const std::string& orow, const std::string& ind) {
+    const GStage& P = g.gs[i];
+    DType dt = p.stages[P.id].dtype;
+    std::string ct = ctype(dt);
+    int esz = dtype_size(dt);
+    o << ind << "const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
+      << ind << "const int oxhi = (cx + PL + OW) < W ? (cx + PL + OW) : W;\n";
+    for (int kk = 0; kk < TX; ++kk) {
+      std::string dst = orow + " + " + std::to_string(32 * V * kk * esz);
+      o << ind << "{\n" << ind << "  " << ct << " w[" << V << "] = {";
+      for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
+      o << "};\n";
+      o << ind << "  const int xs = xL + " << 32 * V * kk << ";\n"
+        << ind << "  if (xs >= oxlo && xs + V <= oxhi) pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n"
+        << ind << "  else if (xs < oxhi && xs + V > oxlo) {\n";
+      for (int v = 0; v < V; ++v)
+        o << ind << "    if (xs + " << v << " >= oxlo && xs + " << v << " < oxhi) reinterpret_cast<" << ct << "*>(" << dst
+          << ")[" << v << "] = w[" << v << "];\n";
+      o << ind << "  }\n" << ind << "}\n";
+    }
   }
 
   // one step of the wavefront: fast = interior tile (no row/column checks); tconst = t known at emit time
@@ -1120,7 +1236,7 @@ struct Emitter {
             o << in3 << sv(i, cur, kk, v) << " = " << conv_store(val, sd.dtype) << ";\n";
           }
       }
-      if (P.xfix && !fast) {
+      if (P.xfix && (!fast || xk)) {
         // border tiles: columns outside [0, W) take the edge value (reading R1)
         o << in3 << "if (xb) {\n";
         for (int side = 0; side < 2; ++side) {
@@ -1216,7 +1332,15 @@ std::string emit_group(const Analysis& A, const Group& g) {
     gb.nsteps = g.TH_b - g.t_first;
   }
   Emitter eb(A, gb);
-  return src + eb.run_border();
+  src += eb.run_border();
+  if (g.TH_x > 0) {   // x-border kernel: interior bodies on TH_x-row tiles of the side tile columns
+    Group gx = g;
+    gx.cfg.TH = g.TH_x;
+    gx.nsteps = g.TH_x - g.t_first;
+    Emitter ex_(A, gx);
+    src += ex_.run_xborder();
+  }
+  return src;
 }
 
 }  // namespace pmg

@@ -91,18 +91,33 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
         ereads.push_back({gr.idx, i, gr.dy, gr.dx});
       } else {
         const Ext3& se = r.src_is_stage ? A.stage_ext[r.src] : A.image_ext[r.src];
-        bool same_yx = se.e[1] == g.ext.e[1] && se.e[2] == g.ext.e[2] && se.has[1] == g.ext.has[1];
         bool plane_ok = r.form[0] == Form::ABSENT || r.form[0] == Form::CONST ||
                         (r.form[0] == Form::UNIT && r.off[0] == 0 && g.ext.has[0] && se.e[0] == g.ext.e[0]);
-        bool stream = same_yx && plane_ok && (r.form[1] == Form::UNIT || r.form[1] == Form::ABSENT) &&
-                      r.form[2] == Form::UNIT && std::abs(r.off[2]) <= 64 && std::abs(yoff()) <= 64;
+        // index forms of y and x: unit (same extent), or the scaled forms 2v+b / (v+b)/2 staged through the
+        // TMA ring like unit reads (alignment & scaling; DESIGN.md §6 "Scaled streams")
+        const bool scale_on = !(getenv("PMG_SCALED") && getenv("PMG_SCALED")[0] == '0');
+        int sy = -1, sx = -1;
+        if (r.form[1] == Form::ABSENT || (r.form[1] == Form::UNIT && se.e[1] == g.ext.e[1])) sy = 0;
+        else if (scale_on && r.form[1] == Form::DOWN2) sy = 1;
+        else if (scale_on && r.form[1] == Form::UP2) sy = 2;
+        if (r.form[2] == Form::UNIT && se.e[2] == g.ext.e[2]) sx = 0;
+        else if (scale_on && r.form[2] == Form::DOWN2) sx = 1;
+        else if (scale_on && r.form[2] == Form::UP2 && k.V % 2 == 0) sx = 2;
+        if (sy != 0 && !se.has[1]) sy = -1;
+        bool stream = plane_ok && sy >= 0 && sx >= 0 && se.has[1] == g.ext.has[1] && std::abs(r.off[2]) <= 64 &&
+                      std::abs(yoff()) <= 64;
         if (stream) {
           int mode = r.form[0] == Form::ABSENT ? 0 : (r.form[0] == Form::UNIT ? 1 : 2);
           int64_t pc = mode == 2 ? std::max<int64_t>(0, std::min<int64_t>(r.off[0], se.e[0] - 1)) : 0;
+          const int by = (int)yoff();
+          const int py = sy == 1 ? (by & 1) : 0;
+          const int vdy = sy == 1 ? (by >> 1) : by;   // offset in the stream's virtual rows
           int si = -1;
           for (size_t q = 0; q < g.streams.size(); ++q) {
             auto& st = g.streams[q];
-            if (st.src_is_stage == r.src_is_stage && st.src == r.src && st.plane_mode == mode && st.plane_const == pc) si = (int)q;
+            if (st.src_is_stage == r.src_is_stage && st.src == r.src && st.plane_mode == mode && st.plane_const == pc &&
+                st.sy == sy && st.py == py && st.sx == sx)
+              si = (int)q;
           }
           if (si < 0) {
             GStream st;
@@ -113,20 +128,23 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
             st.dtype = r.src_is_stage ? p.stages[r.src].dtype : p.images[r.src].dtype;
             st.esz = dtype_size(st.dtype);
             st.tensor_slot = slot_of(r.src_is_stage, r.src);
-            st.dy_min = st.dy_max = (int)yoff();
+            st.sy = sy;
+            st.py = py;
+            st.sx = sx;
+            st.dy_min = st.dy_max = vdy;
             st.dx_min = st.dx_max = (int)r.off[2];
             g.streams.push_back(st);
             si = (int)g.streams.size() - 1;
           }
           auto& st = g.streams[si];
-          st.dy_min = std::min(st.dy_min, (int)yoff());
-          st.dy_max = std::max(st.dy_max, (int)yoff());
+          st.dy_min = std::min(st.dy_min, vdy);
+          st.dy_max = std::max(st.dy_max, vdy);
           st.dx_min = std::min(st.dx_min, (int)r.off[2]);
           st.dx_max = std::max(st.dx_max, (int)r.off[2]);
           gr.kind = RKind::STREAM;
           gr.idx = si;
-          gr.dy = (int)yoff();
-          gr.dx = (int)r.off[2];
+          gr.dy = vdy;
+          gr.dx = (int)r.off[2];   // raw b of the x index form
           sreads.push_back({si, i, gr.dy, gr.dx});
         } else {
           gr.kind = RKind::GATHER;
@@ -177,12 +195,31 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   int align = k.V;
   for (auto& st : g.streams) {
     int a = 16 / st.esz;
-    align = std::max(align, a);
-    st.el = std::max(0, -st.dx_min);
-    st.er = std::max(0, st.dx_max);
-    st.xl = round_up(st.el, std::max(a, k.V));   // vector smem reads of [-el, V+er) stay inside the row
-    st.xr = round_up(st.er, std::max(a, k.V));
-    st.row_elems = g.CW + st.xl + st.xr;
+    align = std::max(align, st.sx == 2 ? 2 * a : a);   // up2: the smem origin cx/2 must stay 16-byte aligned
+    if (st.sx == 1) {
+      // register index q = 2e + b in [dx_min, 2V-2+dx_max], lane base 2V*lane; vector reads of V elements
+      st.el = std::max(0, -st.dx_min);
+      st.er = std::max(0, k.V - 1 + st.dx_max);
+      const int m = std::max(a, k.V);
+      st.xl = round_up(st.el, m);
+      st.xr = round_up(std::max(0, round_up(k.V + st.er, k.V) - 2 * k.V), m);
+      st.row_elems = 2 * g.CW + st.xl + st.xr;
+    } else if (st.sx == 2) {
+      // register index e' = e + b in [-el, V+er), producer column xL/2 + floor(e'/2); lane base (V/2)*lane
+      st.el = std::max(0, -st.dx_min);
+      st.er = std::max(0, st.dx_max);
+      const int h = k.V / 2;
+      st.xl = round_up((st.el + 1) / 2, std::max(a, h));
+      int qend = (k.V + st.er - 1) / 2 + 1;                 // one past the last producer element of lane 0
+      st.xr = round_up(std::max(0, round_up(qend, h) - h), std::max(a, h));
+      st.row_elems = g.CW / 2 + st.xl + st.xr;
+    } else {
+      st.el = std::max(0, -st.dx_min);
+      st.er = std::max(0, st.dx_max);
+      st.xl = round_up(st.el, std::max(a, k.V));   // vector smem reads of [-el, V+er) stay inside the row
+      st.xr = round_up(st.er, std::max(a, k.V));
+      st.row_elems = g.CW + st.xl + st.xr;
+    }
   }
   for (int i = 0; i < n; ++i) {
     GStage& C = g.gs[i];
@@ -193,6 +230,7 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
         C.vr = std::max(C.vr, g.gs[gr.idx].vr + std::max(0, gr.dx));
       } else if (gr.kind == RKind::STREAM) {
         const GStream& st = g.streams[gr.idx];
+        if (st.sx != 0) continue;   // scaled rows are read from smem only (every register index inside the row)
         C.vl = std::max(C.vl, std::max(0, -gr.dx - st.xl));
         C.vr = std::max(C.vr, std::max(0, gr.dx - st.xr));
       }
@@ -220,6 +258,16 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
     g.TH_b = k.TH;
     for (int d = std::min(want, k.TH); d >= 1; --d)
       if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_b = d; break; }
+  }
+  // x-border tiles of interior rows: a third kernel runs the interior bodies with clamped columns on
+  // TH_x-row tiles (short: those tiles are few and latency-bound); not with shared-memory chunks
+  {
+    const char* e = getenv("PMG_XK");
+    int want = e ? atoi(e) : 24;
+    g.TH_x = 0;
+    if (k.S == 0 && want > 0)
+      for (int d = std::min(want, k.TH); d >= 1; --d)
+        if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_x = d; break; }
   }
   // unroll factor for register-window rotation
   int U = 1;

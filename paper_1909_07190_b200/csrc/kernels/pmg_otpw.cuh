@@ -19,13 +19,15 @@ typedef long long i64;
 
 #define PMG_FULL 0xffffffffu
 
-struct PmgTensor {           // one planar [c][y][x] device tensor (40 bytes; mirrored in runtime.cpp)
+struct PmgTensor {           // one planar [c][y][x] device tensor (56 bytes; mirrored in runtime.cpp)
   const char* ptr;
   i64 row_pitch;             // bytes
   i64 plane_pitch;           // bytes
   i64 frame_stride;          // bytes between batch frames (0 for tables / single images)
   int row_base;              // global row index of buffer row 0 (bands)
   int nrows;                 // rows present in the buffer: stores outside [row_base, row_base + nrows) are dropped
+  int H, W;                  // full extent of the tensor's image (rows, columns): clamping of scaled reads
+  int pad0_, pad1_;
 };
 
 // ------------------------------------------------------------------ float semantics (reading R3)

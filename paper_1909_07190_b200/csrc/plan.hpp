@@ -35,6 +35,11 @@ struct GStream {
   int src = -1;
   int plane_mode = 0;     // 0: source has no plane dim; 1: aligned with the tile plane; 2: constant
   int64_t plane_const = 0;
+  // alignment & scaling: index forms per dim.  y: 0 unit (row v+b), 1 down2 (row 2v+b: the
+  // phase-py rows 2r+py as a virtual image, read at r = v + floor(b/2)), 2 up2 (row floor((v+b)/2): the
+  // virtual image U(r) = P(floor(r/2)) read at r = v+b).  x: 0 unit, 1 down2 (register index q = 2e+b over
+  // the producer columns from 2*xL), 2 up2 (register index e+b, producer column floor((xL+e+b)/2)).
+  int sy = 0, py = 0, sx = 0;
   int dy_min = 0, dy_max = 0, dx_min = 0, dx_max = 0;
   int hi = 0, lo = 0, depth = 1;
   int el = 0, er = 0;     // register extension (elements) each side
@@ -79,6 +84,7 @@ struct Group {
   std::vector<std::pair<bool, int>> tensors;  // slot -> (is_stage, id)
   int CW = 0, PL = 0, PR = 0, OW = 0;
   int t_first = 0, nsteps = 0, U = 1;
+  int TH_x = 0;             // tile rows of the x-border kernel (divides TH; 0: x-border tiles go to the border kernel)
   int TH_b = 0;             // tile rows of the border-tile kernel (divides TH; small: border tiles are latency-bound)
   int ring_bytes = 0;       // one ring slot
   int warp_smem = 0;        // bytes of shared memory per warp

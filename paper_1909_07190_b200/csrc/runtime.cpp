@@ -237,17 +237,21 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     check(D.ModuleLoadData(&k.mod, k.bin.cubin.data()), "cuModuleLoadData");
     check(D.ModuleGetFunction(&k.fn, k.mod, g.name.c_str()), "cuModuleGetFunction");
     check(D.ModuleGetFunction(&k.fn_b, k.mod, (g.name + "_b").c_str()), "cuModuleGetFunction");
-    for (CUfunction f : {k.fn, k.fn_b})
-      if (g.block_smem > 48 * 1024)
+    if (g.TH_x > 0) check(D.ModuleGetFunction(&k.fn_x, k.mod, (g.name + "_x").c_str()), "cuModuleGetFunction");
+    for (CUfunction f : {k.fn, k.fn_b, k.fn_x})
+      if (f && g.block_smem > 48 * 1024)
         check(D.FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, g.block_smem), "cuFuncSetAttribute");
     check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm, k.fn, g.cfg.NW * 32, g.block_smem), "occupancy");
     check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm_b, k.fn_b, g.cfg.NW * 32, g.block_smem), "occupancy");
-    if (k.blocks_per_sm < 1 || k.blocks_per_sm_b < 1) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
+    if (k.fn_x)
+      check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm_x, k.fn_x, g.cfg.NW * 32, g.block_smem), "occupancy");
+    if (k.blocks_per_sm < 1 || k.blocks_per_sm_b < 1 || (k.fn_x && k.blocks_per_sm_x < 1)) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
     const FnStats& fb = k.bin.fns[g.name + "_b"];
     js << (gi ? "," : "") << "{\"name\":\"" << g.name << "\",\"regs\":" << k.bin.regs << ",\"spill_stores\":"
        << k.bin.spill_stores << ",\"spill_loads\":" << k.bin.spill_loads << ",\"block_smem\":" << g.block_smem
        << ",\"blocks_per_sm\":" << k.blocks_per_sm << ",\"border_regs\":" << fb.regs << ",\"border_spill_stores\":"
-       << fb.spill_stores << ",\"border_blocks_per_sm\":" << k.blocks_per_sm_b << ",\"cached\":"
+       << fb.spill_stores << ",\"border_blocks_per_sm\":" << k.blocks_per_sm_b << ",\"xborder_regs\":"
+       << (k.fn_x ? k.bin.fns[g.name + "_x"].regs : 0) << ",\"xborder_blocks_per_sm\":" << k.blocks_per_sm_x << ",\"cached\":"
        << (k.bin.from_cache ? "true" : "false") << ",\"compile_s\":" << k.bin.compile_s << "}";
     P->kernels.push_back(std::move(k));
   }
@@ -406,9 +410,9 @@ BandRows band_rows(const Plan& P, int band, int nbands) {
 
 // ------------------------------------------------------------------------------------------ launch
 #pragma pack(push, 1)
-struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, nrows; };
+struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, nrows, H, W, pad0, pad1; };
 #pragma pack(pop)
-static_assert(sizeof(HostTensor) == 40, "PmgTensor mirror");
+static_assert(sizeof(HostTensor) == 56, "PmgTensor mirror");
 
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* ws, CUstream s, int band,
               int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs) {
@@ -472,7 +476,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     } done{D, lanes, lanes ? P.ev_group[gi] : nullptr, gs};
     const int NT = std::max<int>(1, (int)g.tensors.size()), NTAB = std::max(1, P.ntables),
               NP = std::max<int>(1, (int)p.params.size());
-    size_t off_tab = 40 * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
+    size_t off_tab = sizeof(HostTensor) * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
            off_int = off_prm + 4 * NP, size = (off_int + 56 + 7) / 8 * 8;
     std::vector<char> buf(size, 0);
     for (size_t ti = 0; ti < g.tensors.size(); ++ti) {
@@ -508,7 +512,10 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
           t.nrows = (int32_t)(banded ? need.stage[id].hi - need.stage[id].lo : A.stage_ext[id].e[1]);
         }
       }
-      std::memcpy(buf.data() + 40 * ti, &t, 40);
+      const Ext3& te = is_stage ? A.stage_ext[id] : A.image_ext[id];
+      t.H = (int32_t)te.e[1];
+      t.W = (int32_t)te.e[2];
+      std::memcpy(buf.data() + sizeof(HostTensor) * ti, &t, sizeof(HostTensor));
     }
     for (int ti = 0; ti < P.ntables; ++ti) {
       uint64_t ptr = (uint64_t)(uintptr_t)in[P.nimages + ti].ptr;
@@ -534,12 +541,28 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     // interior rectangle: tiles whose whole wavefront stays inside the image / the computed rows
     // (matches the emitted bodies: no clamping, no x fix-up, no row checks needed there)
     int xlm = 0, xrm = 0, himax = 0;
-    for (auto& st : g.streams) { xlm = std::max(xlm, st.xl); xrm = std::max(xrm, st.xr); himax = std::max(himax, st.hi); }
+    for (auto& st : g.streams) {
+      if (st.sx == 0) { xlm = std::max(xlm, st.xl); xrm = std::max(xrm, st.xr); }
+      himax = std::max(himax, st.hi);
+    }
     for (auto& st : g.gs) himax = std::max(himax, st.hi);
     auto cdiv = [](int64_t a, int64_t b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
     auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
     int64_t txA = std::max<int64_t>(0, cdiv(g.PL + xlm, g.OW));
     int64_t txB = std::min<int64_t>(g.ntx, fdiv((int64_t)Wg - g.CW - xrm + g.PL, g.OW) + 1);
+    // scaled streams (emit.cpp xb_scaled): the tile's producer row [origin - xl, + row_elems) inside [0, Wp)
+    auto scaled_in = [&](int64_t tx) {
+      const int64_t cx = tx * g.OW - g.PL;
+      for (auto& st : g.streams) {
+        if (st.sx == 0) continue;
+        const Ext3& se = st.src_is_stage ? A.stage_ext[st.src] : A.image_ext[st.src];
+        const int64_t o0 = (st.sx == 1 ? 2 * cx : (cx >= 0 ? cx / 2 : -((-cx + 1) / 2))) - st.xl;
+        if (o0 < 0 || o0 + st.row_elems > se.e[2]) return false;
+      }
+      return true;
+    };
+    while (txA < txB && !scaled_in(txA)) ++txA;
+    while (txB > txA && !scaled_in(txB - 1)) --txB;
     // interior tile rows: the tiling starts `top` rows below gy0 (a multiple of the border tile height, enough
     // for the rows the wavefront reads above a tile), and holds the whole tiles whose wavefront stays inside
     // the image and the computed rows; the border kernel takes the top and bottom remainders in TH_b-row tiles
@@ -553,32 +576,40 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     const int64_t n_int = (int64_t)nframes * g.npl * nty_i * (txB - txA);
     const int64_t nty_b = (gy1 - gy0 + THb - 1) / THb;
     const int64_t tyA_b = nty_i > 0 ? top / THb : 0, tyB_b = nty_i > 0 ? tyA_b + nty_i * g.cfg.TH / THb : 0;
-    const int64_t n_bdr = (int64_t)nframes * g.npl * (nty_b * g.ntx - (tyB_b - tyA_b) * (txB - txA));
+    // x-border kernel: the side tile columns of the interior rows in TH_x-row tiles; the border kernel then
+    // keeps only the top / bottom remainders (its excluded rectangle spans every column)
+    const bool xk = K.fn_x && g.TH_x > 0 && nty_i > 0 && (txA > 0 || txB < g.ntx);
+    const int64_t nty_x = xk ? nty_i * g.cfg.TH / g.TH_x : 0;
+    const int64_t n_x = xk ? (int64_t)nframes * g.npl * nty_x * (g.ntx - (txB - txA)) : 0;
+    const int64_t bxA = xk ? 0 : txA, bxB = xk ? g.ntx : txB;
+    const int64_t n_bdr = (int64_t)nframes * g.npl * (nty_b * g.ntx - (tyB_b - tyA_b) * (bxB - bxA));
     (void)nty;
     void* args[] = {buf.data()};
     auto launch = [&](CUfunction f, int bps, int64_t nt, CUstream st, const char* what) {
-      const bool bd = f == K.fn_b;
-      int32_t ints[14] = {Hg, Wg, (int32_t)(bd ? gy0 : gy0_i), gy1, (int32_t)(bd ? nty_b : nty_i), (int32_t)g.ntx,
-                          (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0, (int32_t)txA, (int32_t)txB,
-                          (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : nty_i)};
+      const bool bd = f == K.fn_b, xx = f == K.fn_x;
+      int32_t ints[14] = {Hg, Wg, (int32_t)(bd ? gy0 : gy0_i), gy1, (int32_t)(bd ? nty_b : xx ? nty_x : nty_i), (int32_t)g.ntx,
+                          (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0, (int32_t)(bd ? bxA : txA), (int32_t)(bd ? bxB : txB),
+                          (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : xx ? nty_x : nty_i)};
       std::memcpy(buf.data() + off_int, ints, 56);
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
       CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);
       if (r != CUDA_SUCCESS) throw Error(-6, std::string("launch of ") + g.name + what + ": " + cu_err(r));
       ++P.last_launches;
     };
-    if (n_bdr > 0 && n_int > 0) {
+    if ((n_bdr > 0 || n_x > 0) && n_int > 0) {
       // border tiles on the lane's side stream, forked from and joined back into the lane's stream
       check(D.EventRecord(gfork, gs), "cuEventRecord");
       check(D.StreamWaitEvent(gside, gfork, 0), "cuStreamWaitEvent");
-      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
+      if (n_bdr > 0) launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
+      if (n_x > 0) launch(K.fn_x, K.blocks_per_sm_x, n_x, gside, "_x");
       launch(K.fn, K.blocks_per_sm, n_int, gs, "");
       check(D.EventRecord(gjoin, gside), "cuEventRecord");
       check(D.StreamWaitEvent(gs, gjoin, 0), "cuStreamWaitEvent");
     } else if (n_int > 0) {
       launch(K.fn, K.blocks_per_sm, n_int, gs, "");
-    } else if (n_bdr > 0) {
-      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gs, "_b");
+    } else {
+      if (n_bdr > 0) launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gs, "_b");
+      if (n_x > 0) launch(K.fn_x, K.blocks_per_sm_x, n_x, gs, "_x");
     }
     (void)ntiles;
   }

@@ -34,8 +34,8 @@ struct WsTensor {          // workspace placement of an intermediate (materialis
 struct Kernel {
   Compiled bin;
   CUmodule mod = nullptr;
-  CUfunction fn = nullptr, fn_b = nullptr;   // interior tiles / border tiles
-  int blocks_per_sm = 0, blocks_per_sm_b = 0;
+  CUfunction fn = nullptr, fn_b = nullptr, fn_x = nullptr;   // interior tiles / border tiles / x-border tiles
+  int blocks_per_sm = 0, blocks_per_sm_b = 0, blocks_per_sm_x = 0;
 };
 
 struct Plan {

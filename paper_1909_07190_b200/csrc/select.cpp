@@ -83,6 +83,9 @@ static double ops_of(const Expr& e) {
   for (auto& a : e.args) c += ops_of(*a);
   switch (e.op) {
     case Expr::BIN:
+      if ((e.text == "/" || e.text == "%") && e.kind == Kind::Int && e.args[1]->op == Expr::INT && e.args[1]->ival >= 2 &&
+          (e.args[1]->ival & (e.args[1]->ival - 1)) == 0)
+        return c + 1;   // shift / mask (emit.cpp)
       if (e.text == "/") return c + (e.kind == Kind::Float ? 8 : 20);
       if (e.text == "%") return c + 20;
       return c + 1;
@@ -146,13 +149,14 @@ static double min_txs(int64_t start, int64_t nbytes, int tx) {
 // (profiles/sweep_r01_*.txt, tools/fit_weights.py).
 struct TimeModel {
   double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1800, launch_us = 1, c_border = 3, cpi_warp = 4;
+  double c_gather = 12;   // per gathered read per point (camera / pyramid sweeps)
 };
 static TimeModel time_model() {
   TimeModel m;
   if (const char* e = getenv("PMG_TM")) {     // calibration hook: "c0,c_stage,c_stream,lat_cycles,launch_us,c_border,cpi_warp"
     double v[7];
     if (sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6]) == 7)
-      m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5], v[6]};
+      m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5], v[6], m.c_gather};
   }
   return m;
 }
@@ -188,6 +192,10 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   const double tiles = C * std::ceil(H / k.TH) * std::ceil(W / g.OW);
   double ops = 0;
   for (auto& P : g.gs) ops += std::max(1.0, body_ops(*p.stages[P.id].expr));
+  // a gathered read (per-element clamped global load, not staged through the TMA ring) costs its index
+  // arithmetic and an exposed L2 round trip that the ring would have hidden
+  for (auto& r : g.greads)
+    if (r.kind == RKind::GATHER) ops += M.c_gather;
   const double I_step = k.V * k.TX * ops + k.TX * (M.c_stage * g.gs.size() + M.c_stream * g.streams.size()) + M.c0;
   const double R = std::max(1.0, std::floor(resident_warps));
   const double lat = M.lat_cycles * 4.0 / std::max(1, k.PREF);
@@ -565,7 +573,7 @@ std::string config_json(const Analysis& A, const Group& g) {
     auto& S = g.streams[j];
     o << (j ? "," : "") << "{\"src\":\"" << (S.src_is_stage ? p.stages[S.src].name : p.images[S.src].name)
       << "\",\"plane_mode\":" << S.plane_mode << ",\"hi\":" << S.hi << ",\"lo\":" << S.lo << ",\"window\":" << S.depth
-      << ",\"smem_ext\":[" << S.xl << "," << S.xr << "]}";
+      << ",\"smem_ext\":[" << S.xl << "," << S.xr << "],\"scale\":[" << S.sy << "," << S.py << "," << S.sx << "]}";
   }
   int ng = 0;
   for (auto& r : g.greads) ng += r.kind == RKind::GATHER;

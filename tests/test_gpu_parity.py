@@ -118,3 +118,23 @@ def test_local_laplacian_small_parity():
     exp = evaluate(w.text, w.params, inp)
     got, _ = run_gpu(w.text, w.params, inp)
     compare(got["out"], exp["out"], float_tol=1e-4)
+
+
+SCALED = [dict(vec=v, chunks=tx, rows=th, warps=1, prefetch=pf)
+          for (v, tx, th, pf) in [(1, 1, 3, 2), (2, 1, 8, 4), (2, 2, 5, 3), (4, 1, 16, 4), (4, 2, 8, 2), (4, 4, 4, 4)]]
+
+
+@pytest.mark.parametrize("cfg", SCALED, ids=lambda c: "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
+@pytest.mark.parametrize("W,H", [(97, 63), (256, 130), (1201, 77)])
+def test_scaled_streams(cfg, W, H):
+    """Alignment & scaling: 2v+b and (v+b)/2 reads staged through the TMA ring as scaled streams
+     on odd and even extents, every lane width; bit-exact against the oracle."""
+    from pathlib import Path
+    text = (Path(__file__).parent / "golden" / "scaled_streams.pmg").read_text()
+    img = PI.uniform((H, W), 77)
+    exp = evaluate(text, {"W": W, "H": H}, {"img": img})
+    got, plan = run_gpu(text, {"W": W, "H": H}, {"img": img}, opts=pmg.sched_opts(**cfg, tx_size=32))
+    neq, _ = compare(got["u"], exp["u"], float_tol=1e-4)
+    assert neq == 0
+    assert any(s.get("scale", [0, 0, 0]) != [0, 0, 0] for g in plan.describe()["schedule"]["groups"]
+               for s in g["config"]["streams"]), "no scaled stream in the plan"
