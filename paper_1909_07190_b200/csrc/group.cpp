@@ -259,11 +259,12 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
     for (int d = std::min(want, k.TH); d >= 1; --d)
       if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_b = d; break; }
   }
-  // x-border tiles of interior rows: a third kernel runs the interior bodies with clamped columns on
-  // TH_x-row tiles (short: those tiles are few and latency-bound); not with shared-memory chunks
+  // x-border tiles of interior rows: optionally (PMG_XK = rows) a third kernel runs the interior bodies with
+  // clamped columns on TH_x-row tiles; not with shared-memory chunks.  Off by default: measured slower on
+  // B200 for every workload (profiles/xborder_kernel_r01f.txt)
   {
     const char* e = getenv("PMG_XK");
-    int want = e ? atoi(e) : 24;
+    int want = e ? atoi(e) : 0;
     g.TH_x = 0;
     if (k.S == 0 && want > 0)
       for (int d = std::min(want, k.TH); d >= 1; --d)
