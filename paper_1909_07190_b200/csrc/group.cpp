@@ -95,7 +95,7 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
                         (r.form[0] == Form::UNIT && r.off[0] == 0 && g.ext.has[0] && se.e[0] == g.ext.e[0]);
         // index forms of y and x: unit (same extent), or the scaled forms 2v+b / (v+b)/2 staged through the
         // TMA ring like unit reads (alignment & scaling; DESIGN.md §6 "Scaled streams")
-        const bool scale_on = !(getenv("PMG_SCALED") && getenv("PMG_SCALED")[0] == '0');
+        const bool scale_on = !g.no_scaled && !(getenv("PMG_SCALED") && getenv("PMG_SCALED")[0] == '0');
         int sy = -1, sx = -1;
         if (r.form[1] == Form::ABSENT || (r.form[1] == Form::UNIT && se.e[1] == g.ext.e[1])) sy = 0;
         else if (scale_on && r.form[1] == Form::DOWN2) sy = 1;
@@ -153,6 +153,17 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
       }
       g.read_map[ri] = (int)g.greads.size();
       g.greads.push_back(gr);
+    }
+  }
+  // every stream keeps ~6 registers of per-tile refill state; a group that would read many scaled inputs
+  // (the camera interleave: 12 quad planes) reads them by gather instead (measured: 232-247 registers with
+  // 12 scaled streams, profiles/scaled_streams_r01e.txt)
+  {
+    int nscaled = 0;
+    for (auto& st : g.streams) nscaled += (st.sy != 0 || st.sx != 0);
+    if (nscaled > 4 && !g.no_scaled) {
+      g.no_scaled = true;
+      return build_group(A, g, gos);
     }
   }
   // row reach (right hyperplane in y) and overlaps, backward over topo order

@@ -149,14 +149,14 @@ static double min_txs(int64_t start, int64_t nbytes, int tx) {
 // (profiles/sweep_r01_*.txt, tools/fit_weights.py).
 struct TimeModel {
   double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1800, launch_us = 1, c_border = 3, cpi_warp = 4;
-  double c_gather = 12;   // per gathered read per point (camera / pyramid sweeps)
+  double c_gather = 6;    // per gathered read per point (camera sweeps 3 / 6 / 12: profiles/camera_groupings_r01g.txt)
 };
 static TimeModel time_model() {
   TimeModel m;
-  if (const char* e = getenv("PMG_TM")) {     // calibration hook: "c0,c_stage,c_stream,lat_cycles,launch_us,c_border,cpi_warp"
-    double v[7];
-    if (sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6]) == 7)
-      m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5], v[6], m.c_gather};
+  if (const char* e = getenv("PMG_TM")) {     // calibration hook: "c0,c_stage,c_stream,lat_cycles,launch_us,c_border,cpi_warp[,c_gather]"
+    double v[8];
+    int n = sscanf(e, "%lf,%lf,%lf,%lf,%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &v[7]);
+    if (n >= 7) m = TimeModel{v[0], v[1], v[2], v[3], v[4], v[5], v[6], n == 8 ? v[7] : m.c_gather};
   }
   return m;
 }
