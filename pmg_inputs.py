@@ -9,7 +9,7 @@ Workload recipe (DESIGN.md §"Inputs"): shapes/dtypes are BASELINE.json's config
 U[0,1) i.i.d. f32 for the float pipelines plus structured variants (gradients, rectangles, flat patches,
 noise) where the pipeline has data-dependent control flow; camera raw is a GRBG mosaic of a synthetic
 scene with sigma=8 DN noise and 0.01 % hot pixels, 10-bit.  Seeds: C1 1001, C2 1002, C3 1003, C4 1004,
-C5 1005.
+C5 1005, PB 1006 (A) / 1007 (B).
 """
 from __future__ import annotations
 
@@ -45,6 +45,12 @@ def structured(shape, seed):
         img = np.where(flat, 0.5, img)
         out[idx] = np.clip(img, 0.0, 1.0).astype(np.float32)
     return out
+
+
+def blend_mask(h, w):
+    """Pyramid-blend mask: 0 on the left, 1 on the right, a linear ramp over the middle eighth of the width."""
+    x = (np.arange(w, dtype=np.float64) - (w - 1) / 2.0) / max(1.0, w / 8.0) + 0.5
+    return np.broadcast_to(np.clip(x, 0.0, 1.0)[None, :], (h, w)).astype(np.float32).copy()
 
 
 def bayer_raw(h, w, seed, black=25, white=1023):
@@ -132,6 +138,9 @@ class Workload:
             K = 8 if self.pipeline == "local_laplacian.pmg" else int(self.pipeline.split("K")[-1].split(".")[0])
             img = structured((3, H, W), s) if variant != "uniform" else uniform((3, H, W), s)
             return {"inp": img, "remap": ll_remap(K)}
+        if self.pipeline.startswith("pyramid_blend"):
+            return {"A": structured((3, H, W), s), "B": structured((3, H, W), s + 1) if variant != "uniform"
+                    else uniform((3, H, W), s + 1), "M": blend_mask(H, W)}
         if self.pipeline == "unsharp.pmg":
             img = structured((3, H, W), s) if variant != "uniform" else uniform((3, H, W), s)
             return {"img": img}
@@ -151,6 +160,9 @@ WORKLOADS = {
     "camera": Workload("camera", "camera.pmg", {"W": 2528, "H": 1920}, 1004, "C4 2528x1920 u16 Bayer"),
     "local_laplacian": Workload("local_laplacian", "local_laplacian.pmg", {"W": 2560, "H": 1536}, 1005,
                                 "C5 2560x1536x3 f32, J=8, K=8"),
+    # PAPER.md Table 2 l.1150 (not a BASELINE.json config)
+    "pyramid_blend": Workload("pyramid_blend", "pyramid_blend.pmg", {"W": 3840, "H": 2160}, 1006,
+                              "PB 3840x2160x3 f32, J=4"),
 }
 
 

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 import paper_1909_07190_b200 as pmg  # noqa: E402
 
 TOL = {"blur": dict(float_tol=1e-4), "unsharp": dict(float_tol=1e-4), "harris": dict(rel_range=1e-5),
-       "local_laplacian": dict(float_tol=1e-4), "camera": {}}
+       "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4)}
 
 
 def sample_points(shape, n, seed):
@@ -33,18 +33,18 @@ def sample_points(shape, n, seed):
     return tuple(c.astype(np.int64) for c in cols)
 
 
-@pytest.mark.parametrize("name", ["harris", "unsharp", "camera", "blur", "local_laplacian"])
+@pytest.mark.parametrize("name", ["harris", "unsharp", "camera", "blur", "local_laplacian", "pyramid_blend"])
 def test_fullsize_sampled_parity(name):
     import torch
     wl = PI.WORKLOADS[name]
-    inp = wl.inputs("structured") if name == "local_laplacian" else wl.inputs()
+    inp = wl.inputs("structured") if name in ("local_laplacian", "pyramid_blend") else wl.inputs()
     plan = pmg.Plan(pmg.Pipeline(wl.text), wl.params)              # automatic schedule, as bench.py
     ins = [to_device(inp[io.name], io.dtype, pitched=not io.is_table) for io in plan.inputs]
     outs = plan.run(ins)
     torch.cuda.synchronize()
     (io, out), = zip(plan.outputs, outs)
     got = to_numpy(out)
-    pts = sample_points(got.shape, 24 if name == "local_laplacian" else 96, seed=11)
+    pts = sample_points(got.shape, 24 if name in ("local_laplacian", "pyramid_blend") else 96, seed=11)
     exp = evaluate_points(wl.text, wl.params, inp, io.name, pts)
     neq, d = compare(np.ascontiguousarray(got[pts]), exp, **TOL[name])
     assert neq == 0, f"{name}: {neq} sampled outputs differ from the oracle (max {d})"

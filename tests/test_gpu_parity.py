@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 import paper_1909_07190_b200 as pmg  # noqa: E402
 
 TOL = {"blur": dict(float_tol=1e-4), "unsharp": dict(float_tol=1e-4), "harris": dict(rel_range=1e-5),
-       "local_laplacian": dict(float_tol=1e-4), "camera": {}}
+       "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4)}
 
 
 def check(name, W, H, opts=None, variant="uniform", bit_exact=True):
@@ -138,3 +138,17 @@ def test_scaled_streams(cfg, W, H):
     assert neq == 0
     assert any(s.get("scale", [0, 0, 0]) != [0, 0, 0] for g in plan.describe()["schedule"]["groups"]
                for s in g["config"]["streams"]), "no scaled stream in the plan"
+
+
+@pytest.mark.parametrize("cfg", [None] + PARITY_SWEEP[:4],
+                         ids=lambda c: "auto" if c is None else "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
+@pytest.mark.parametrize("W,H", [(97, 63), (256, 130)])
+def test_pyramid_blend_parity(cfg, W, H):
+    """Pyramid Blend (Table 2): three Gaussian pyramids, two Laplacian pyramids,
+    per-level blend and collapse through scaled streams, inlined upsamplings and broadcast mask reads."""
+    w = PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": W, "H": H}, 1006)
+    inp = w.inputs("structured")
+    exp = evaluate(w.text, w.params, inp)
+    got, _ = run_gpu(w.text, w.params, inp, opts=None if cfg is None else pmg.sched_opts(**cfg, tx_size=32))
+    neq, _ = compare(got["out"], exp["out"], float_tol=1e-4)
+    assert neq == 0

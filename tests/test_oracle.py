@@ -204,9 +204,55 @@ def test_local_laplacian_shapes_and_stage_count():
     assert ev.shape_of("gP7") == (8, 12, 20) and ev.shape_of("out") == (3, 1536, 2560)
 
 
+# ----------------------------------------------------------------------------- pyramid blend (NEXT-4)
+def _pb(W=64, H=48):
+    return (PI.PIPELINES / "pyramid_blend_J3.pmg").read_text(), {"W": W, "H": H}
+
+
+@pytest.mark.parametrize("which", ["ones", "zeros"])
+def test_pyramid_blend_constant_mask_reconstructs_one_image(which):
+    """Mask == 1 (resp. 0): every blended level is lA_j (lB_j) exactly, and the Laplacian collapse
+    telescopes back to A (B): oG_j = up(oG_{j+1}) + XG_j - up(XG_{j+1}) = XG_j by induction (exact
+    arithmetic; f64 mode)."""
+    text, p = _pb()
+    A, B = PI.uniform((3, 48, 64), 3), PI.uniform((3, 48, 64), 4)
+    M = np.full((48, 64), 1.0 if which == "ones" else 0.0, np.float32)
+    out = evaluate(text, p, {"A": A, "B": B, "M": M}, precision="f64")["out"]
+    np.testing.assert_allclose(out, (A if which == "ones" else B).astype(np.float64), rtol=0, atol=1e-12)
+
+
+def test_pyramid_blend_identical_images_ignore_the_mask():
+    text, p = _pb()
+    A = PI.uniform((3, 48, 64), 5)
+    out = evaluate(text, p, {"A": A, "B": A, "M": PI.uniform((48, 64), 6)}, precision="f64")["out"]
+    np.testing.assert_allclose(out, A.astype(np.float64), rtol=0, atol=1e-12)
+
+
+def test_pyramid_blend_down_up_of_ramp():
+    """[1 3 3 1]/8 downsample of a ramp a*x is a*(2x+0.5); the (x+1)/2, (x-1)/2 linear upsample maps a
+    coarse ramp back to a*(x-0.5)/2, so lA0 = AG0 - up(AG1) vanishes away from the border."""
+    text, p = _pb()
+    yy, xx = np.mgrid[0:48, 0:64]
+    g = ((xx + 2 * yy) / 1024.0 + 0.125).astype(np.float32)
+    A = np.stack([g, g, g])
+    st = evaluate(text, p, {"A": A, "B": A, "M": np.zeros((48, 64), np.float32)}, precision="f64", keep_all=True)
+    xs = 2 * np.arange(32) + 0.5
+    np.testing.assert_allclose(st["ADx1"][0][:, 1:-1], ((xs[None, :] + 2 * np.arange(48)[:, None]) / 1024.0 + 0.125)[:, 1:-1],
+                               rtol=0, atol=1e-12)
+    assert np.max(np.abs(st["lA0"][:, 3:-3, 3:-3])) < 1e-12
+
+
+def test_pyramid_blend_shapes_and_stage_count():
+    prog = parse((PI.PIPELINES / "pyramid_blend.pmg").read_text())
+    assert len(prog.stages) == 41
+    ev = Evaluator(prog, {"W": 3840, "H": 2160})
+    assert ev.shape_of("AG3") == (3, 270, 480) and ev.shape_of("MG3") == (270, 480)
+    assert ev.shape_of("out") == (3, 2160, 3840)
+
+
 # ----------------------------------------------------------------------------- f32 vs exact arithmetic
 @pytest.mark.parametrize("name,W,H,tol", [("blur", 40, 30, 1e-6), ("unsharp", 40, 30, 1e-5),
-                                          ("harris", 40, 30, None)])
+                                          ("harris", 40, 30, None), ("pyramid_blend", 64, 48, 1e-5)])
 def test_f32_within_tolerance_of_exact(name, W, H, tol):
     w = PI.small(name, W, H)
     inp = w.inputs()
@@ -320,7 +366,8 @@ def test_golden_digests_unchanged():
 # ------------------------------------------------------------------ demand-driven (sampled) oracle
 @pytest.mark.parametrize("wl", [PI.small("blur", 70, 50), PI.small("harris", 90, 61), PI.small("unsharp", 64, 40),
                                 PI.small("camera", 96, 64),
-                                PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005)],
+                                PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005),
+                                PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 70, "H": 46}, 1006)],
                          ids=lambda w: w.pipeline)
 def test_point_oracle_equals_whole_domain(wl):
     """oracle/points.py restates the definition at requested points only (used at BASELINE sizes); it must
