@@ -95,7 +95,9 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
                         (r.form[0] == Form::UNIT && r.off[0] == 0 && g.ext.has[0] && se.e[0] == g.ext.e[0]);
         // index forms of y and x: unit (same extent), or the scaled forms 2v+b / (v+b)/2 staged through the
         // TMA ring like unit reads (alignment & scaling; DESIGN.md §6 "Scaled streams")
-        const bool scale_on = !g.no_scaled && !(getenv("PMG_SCALED") && getenv("PMG_SCALED")[0] == '0');
+        // opt-in (PMG_SCALED=1): measured 3 % slower than L1/L2-served gathers on every pyramid workload
+        // (camera 0.151 vs 0.147, local Laplacian 0.396 vs 0.381, pyramid blend 0.479 vs 0.465 ms)
+        const bool scale_on = !g.no_scaled && getenv("PMG_SCALED") && getenv("PMG_SCALED")[0] == '1';
         int sy = -1, sx = -1;
         if (r.form[1] == Form::ABSENT || (r.form[1] == Form::UNIT && se.e[1] == g.ext.e[1])) sy = 0;
         else if (scale_on && r.form[1] == Form::DOWN2) sy = 1;

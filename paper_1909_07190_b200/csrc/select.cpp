@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <map>
 #include <sstream>
@@ -183,6 +184,49 @@ static double body_ops(const Expr& e) {
   }
 }
 
+// `cond` tests the parity of the stage's x variable (x % 2 ... with only x and literals): with even V the
+// emitter folds it per element (emit.cpp x_even), so only one branch of the select is evaluated
+static bool x_parity_test(const Expr& e, int nd) {
+  std::function<bool(const Expr&)> only_x = [&](const Expr& q) {
+    if (q.op == Expr::INT) return true;
+    if (q.op == Expr::VAR) return q.index + 3 - nd == 2;
+    if (q.op == Expr::BIN && (q.text == "+" || q.text == "-")) return only_x(*q.args[0]) && only_x(*q.args[1]);
+    return false;
+  };
+  std::function<bool(const Expr&)> has_mod = [&](const Expr& q) {
+    if (q.op == Expr::BIN && q.text == "%" && q.args[1]->op == Expr::INT && q.args[1]->ival == 2 && only_x(*q.args[0])) return true;
+    for (auto& a : q.args)
+      if (has_mod(*a)) return true;
+    return false;
+  };
+  if (e.op != Expr::BIN || (e.text != "==" && e.text != "!=")) return false;
+  for (int s = 0; s < 2; ++s)
+    if (has_mod(*e.args[s]) && (e.args[1 - s]->op == Expr::INT)) return true;
+  return false;
+}
+
+// body instructions per point with the x-parity selects resolved (even V) and each gathered read charged
+// c_gather (reads through registers / shuffles / the TMA ring cost nothing here)
+static double eval_cost(const Expr& e, int nd, bool xeven, double c_gather, const std::map<const Expr*, RKind>& kinds) {
+  if (e.op == Expr::ACCESS) {
+    double c = 0;
+    auto it = kinds.find(&e);
+    if (it != kinds.end() && it->second == RKind::GATHER) c += c_gather;
+    return c;   // index expressions are resolved at compile time or folded into the gather's address
+  }
+  if (e.op == Expr::CALL && e.text == "select" && xeven && x_parity_test(*e.args[0], nd))
+    return std::max(eval_cost(*e.args[1], nd, xeven, c_gather, kinds), eval_cost(*e.args[2], nd, xeven, c_gather, kinds));
+  double c = 0;
+  for (auto& a : e.args) c += eval_cost(*a, nd, xeven, c_gather, kinds);
+  if (e.op == Expr::BIN || e.op == Expr::UN || e.op == Expr::CALL || e.op == Expr::TABLE) {
+    // the node's own cost as body_ops counts it (children excluded)
+    double self = body_ops(e);
+    for (auto& a : e.args) self -= body_ops(*a);
+    c += self;
+  }
+  return c;
+}
+
 static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec& S, double resident_warps,
                           CostBreakdown* rec = nullptr, int bands = 1) {
   static const TimeModel M = time_model();
@@ -190,12 +234,16 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   const KConfig& k = g.cfg;
   const double H = std::ceil((double)g.ext.e[1] / std::max(1, bands)), W = (double)g.ext.e[2], C = (double)g.npl;
   const double tiles = C * std::ceil(H / k.TH) * std::ceil(W / g.OW);
-  double ops = 0;
-  for (auto& P : g.gs) ops += std::max(1.0, body_ops(*p.stages[P.id].expr));
   // a gathered read (per-element clamped global load, not staged through the TMA ring) costs its index
-  // arithmetic and an exposed L2 round trip that the ring would have hidden
-  for (auto& r : g.greads)
-    if (r.kind == RKind::GATHER) ops += M.c_gather;
+  // arithmetic and an exposed L2 round trip that the ring would have hidden (c_gather per read per point)
+  std::map<const Expr*, RKind> kinds;
+  for (auto& P : g.gs)
+    for (int ri : A.reads_of[P.id])
+      if (g.read_map[ri] >= 0) kinds[A.reads[ri].node] = g.greads[g.read_map[ri]].kind;
+  const bool xeven = k.V % 2 == 0 && g.OW % 2 == 0 && g.PL % 2 == 0;
+  double ops = 0;
+  for (auto& P : g.gs)
+    ops += std::max(1.0, eval_cost(*p.stages[P.id].expr, (int)p.stages[P.id].vars.size(), xeven, M.c_gather, kinds));
   const double I_step = k.V * k.TX * ops + k.TX * (M.c_stage * g.gs.size() + M.c_stream * g.streams.size()) + M.c0;
   const double R = std::max(1.0, std::floor(resident_warps));
   const double lat = M.lat_cycles * 4.0 / std::max(1, k.PREF);

@@ -126,10 +126,11 @@ SCALED = [dict(vec=v, chunks=tx, rows=th, warps=1, prefetch=pf)
 
 @pytest.mark.parametrize("cfg", SCALED, ids=lambda c: "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
 @pytest.mark.parametrize("W,H", [(97, 63), (256, 130), (1201, 77)])
-def test_scaled_streams(cfg, W, H):
+def test_scaled_streams(cfg, W, H, monkeypatch):
     """Alignment & scaling: 2v+b and (v+b)/2 reads staged through the TMA ring as scaled streams
-     on odd and even extents, every lane width; bit-exact against the oracle."""
+    (opt-in PMG_SCALED=1) on odd and even extents, every lane width; bit-exact against the oracle."""
     from pathlib import Path
+    monkeypatch.setenv("PMG_SCALED", "1")
     text = (Path(__file__).parent / "golden" / "scaled_streams.pmg").read_text()
     img = PI.uniform((H, W), 77)
     exp = evaluate(text, {"W": W, "H": H}, {"img": img})
@@ -152,3 +153,18 @@ def test_pyramid_blend_parity(cfg, W, H):
     got, _ = run_gpu(w.text, w.params, inp, opts=None if cfg is None else pmg.sched_opts(**cfg, tx_size=32))
     neq, _ = compare(got["out"], exp["out"], float_tol=1e-4)
     assert neq == 0
+
+
+@pytest.mark.parametrize("name", ["camera", "pyramid_blend"])
+def test_scaled_streams_on_pipelines(name, monkeypatch):
+    """The scaled-stream path on the camera pipe (Bayer phases: 2v+b in y and x) and the pyramid blend."""
+    monkeypatch.setenv("PMG_SCALED", "1")
+    w = PI.small(name, 263, 131) if name == "camera" else PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 97, "H": 63}, 1006)
+    inp = w.inputs("structured") if name != "camera" else w.inputs()
+    exp = evaluate(w.text, w.params, inp)
+    got, plan = run_gpu(w.text, w.params, inp, opts=pmg.sched_opts(vec=2, chunks=2, rows=8, warps=1, prefetch=4, tx_size=32))
+    for k in exp:
+        neq, _ = compare(got[k], exp[k], float_tol=1e-4)
+        assert neq == 0
+    assert any(s.get("scale", [0, 0, 0]) != [0, 0, 0] for g in plan.describe()["schedule"]["groups"]
+               for s in g["config"]["streams"])
