@@ -122,7 +122,12 @@ typedef struct {
                            counts the tiles of one band; <= 1 = whole image */
   int32_t no_inline;    /* 0 (default): substitute data-expanding intermediate stages into their readers
                            (a B200 option outside the paper); 1: schedule the text as written */
-  int32_t reserved[2];
+  int32_t tune;         /* 0 (default): the model's schedule.  1: measured selection on the plan's device -- the
+                           DP schedule and every schedule that merges two neighbouring groups of it are compiled,
+                           run on synthetic inputs and timed (CUDA events); the fastest is kept.  Plan creation
+                           then takes seconds per candidate; runs are unaffected.  A B200 refinement outside the
+                           paper's model-based selector. */
+  int32_t reserved;
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);

@@ -345,7 +345,9 @@ void pmg_plan_destroy(pmg_plan plan) {
 
 pmg_status pmg_plan_describe(pmg_plan plan, char* buf, size_t cap, size_t* needed) {
   if (!plan) return fail(PMG_ERR_ARG, "NULL plan");
-  return put_json(plan->plan->json, buf, cap, needed);
+  std::string j = plan->plan->json;
+  if (!plan->plan->tune_json.empty()) j = j.substr(0, j.size() - 1) + ",\"tune\":" + plan->plan->tune_json + "}";
+  return put_json(j, buf, cap, needed);
 }
 
 pmg_status pmg_plan_workspace_bytes(pmg_plan plan, size_t* out) {

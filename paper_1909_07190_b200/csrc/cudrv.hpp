@@ -43,6 +43,9 @@ struct Drv {
   CUresult (*StreamWaitEvent)(CUstream, CUevent, unsigned);
   CUresult (*Memcpy2DAsync)(const CUDA_MEMCPY2D*, CUstream);
   CUresult (*MemcpyHtoDAsync)(CUdeviceptr, const void*, size_t, CUstream);
+  CUresult (*EventSynchronize)(CUevent);
+  CUresult (*EventElapsedTime)(float*, CUevent, CUevent);
+  CUresult (*MemsetD8)(CUdeviceptr, unsigned char, size_t);
 };
 
 inline Drv& drv() {
@@ -89,6 +92,9 @@ inline Drv& drv() {
     PMG_SYM(StreamWaitEvent, "cuStreamWaitEvent");
     PMG_SYM(Memcpy2DAsync, "cuMemcpy2DAsync_v2");
     PMG_SYM(MemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2");
+    PMG_SYM(EventSynchronize, "cuEventSynchronize");
+    PMG_SYM(EventElapsedTime, "cuEventElapsedTime");
+    PMG_SYM(MemsetD8, "cuMemsetD8_v2");
 #undef PMG_SYM
     if (!all) { d.err = "CUDA driver is missing required symbols"; return; }
     CUresult r = d.Init(0);

@@ -167,10 +167,96 @@ struct CtxGuard {   // make the plan's primary context current for the duration 
 
 static int64_t round_up64(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 
+// device time of one run of plan Q on synthetic inputs (measured selection, pmg_sched_opts.tune): buffers
+// are allocated here, filled with a constant byte pattern, 2 warm-up runs then the mean of 5 timed runs
+static double time_plan_us(Plan& Q) {
+  Drv& D = drv();
+  const Pipeline& p = *Q.pipe;
+  const Analysis& A = Q.A;
+  std::vector<CUdeviceptr> mem;
+  struct Free {
+    Drv& D; std::vector<CUdeviceptr>& m;
+    ~Free() { for (auto x : m) D.MemFree(x); }
+  } free_all{D, mem};
+  auto alloc = [&](size_t bytes) {
+    CUdeviceptr d = 0;
+    check(D.MemAlloc(&d, std::max<size_t>(bytes, 256)), "cuMemAlloc");
+    mem.push_back(d);
+    check(D.MemsetD8(d, 0x3c, std::max<size_t>(bytes, 256)), "cuMemsetD8");   // 0x3c3c3c3c = 0.0115f
+    return d;
+  };
+  auto buf_of = [&](const Ext3& e, DType dt) {
+    pmg_buf b{};
+    b.row_pitch_bytes = round_up64(e.e[2] * dtype_size(dt), 128);
+    b.plane_pitch_bytes = b.row_pitch_bytes * e.e[1];
+    b.ptr = (void*)(uintptr_t)alloc((size_t)(b.plane_pitch_bytes * e.e[0]));
+    return b;
+  };
+  std::vector<pmg_buf> in, out;
+  for (size_t i = 0; i < p.images.size(); ++i) in.push_back(buf_of(A.image_ext[i], p.images[i].dtype));
+  for (size_t i = 0; i < p.tables.size(); ++i) {
+    pmg_buf b{};
+    b.ptr = (void*)(uintptr_t)alloc((size_t)A.table_len[i] * dtype_size(p.tables[i].dtype));
+    in.push_back(b);
+  }
+  for (int s : p.liveouts) out.push_back(buf_of(A.stage_ext[s], p.stages[s].dtype));
+  void* ws = Q.ws_bytes ? (void*)(uintptr_t)alloc(Q.ws_bytes) : nullptr;
+  CUstream st;
+  check(D.StreamCreate(&st, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  CUevent e0, e1;
+  check(D.EventCreate(&e0, 0), "cuEventCreate");
+  check(D.EventCreate(&e1, 0), "cuEventCreate");
+  for (int r = 0; r < 2; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, -1, 0, 1, nullptr, nullptr);
+  check(D.EventRecord(e0, st), "cuEventRecord");
+  const int R = 5;
+  for (int r = 0; r < R; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, -1, 0, 1, nullptr, nullptr);
+  check(D.EventRecord(e1, st), "cuEventRecord");
+  check(D.EventSynchronize(e1), "cuEventSynchronize");
+  float ms = 0;
+  check(D.EventElapsedTime(&ms, e0, e1), "cuEventElapsedTime");
+  D.EventDestroy(e0);
+  D.EventDestroy(e1);
+  D.StreamDestroy(st);
+  return 1000.0 * ms / R;
+}
+
 std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,
                                   const pmg_gpu_spec* spec, const pmg_weights* w, const pmg_sched_opts* opts) {
   Drv& D = drv();
   if (!D.ok) throw Error(-6, D.err);
+  if (opts && opts->tune > 0 && !opts->group_of_stage) {
+    // measured selection: the model's plan, then every neighbour merge of its groups; keep the fastest
+    pmg_sched_opts o0 = *opts;
+    o0.tune = 0;
+    std::unique_ptr<Plan> best = plan_create(p, params, device, spec, w, &o0);
+    std::vector<std::vector<int>> cands;
+    {
+      CtxGuard g(best->ctx);
+      cands = merge_candidates(best->A, best->sch);
+      double tb = time_plan_us(*best);
+      std::ostringstream js;
+      js << "{\"candidates\":[{\"groups\":" << best->sch.groups.size() << ",\"us\":" << tb << "}";
+      int chosen = 0, pos = 0;
+      for (size_t c = 1; c < cands.size(); ++c) {
+        pmg_sched_opts oc = o0;
+        oc.group_of_stage = cands[c].data();
+        std::unique_ptr<Plan> Q;
+        try {
+          Q = plan_create(p, params, device, spec, w, &oc);
+        } catch (const Error&) {
+          continue;   // a merge the geometry cannot build (e.g. a non-constant dependence)
+        }
+        CtxGuard gq(Q->ctx);
+        double t = time_plan_us(*Q);
+        js << ",{\"groups\":" << Q->sch.groups.size() << ",\"us\":" << t << "}";
+        ++pos;
+        if (t < tb) { tb = t; best = std::move(Q); chosen = pos; }
+      }
+      js << "],\"chosen\":" << chosen << "}";
+      best->tune_json = js.str();
+    }
+    return best;
+  }
   auto P = std::make_unique<Plan>();
   if (!(opts && opts->no_inline)) p = inline_expanding(p, params, &P->inlined);
   P->pipe = p;

@@ -62,6 +62,7 @@ struct Plan {
   std::vector<CUstream> lane_stream, lane_side;
   std::vector<CUevent> lane_fork, lane_join, ev_group;
   CUevent ev_run = nullptr;
+  std::string tune_json;                   // measured selection report (pmg_sched_opts.tune), empty otherwise
   int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
   // host-buffer runs (pmg_run_host): copy streams and per-chunk events, created on first use
   CUstream h2d = nullptr, d2h = nullptr;

@@ -743,4 +743,20 @@ std::string paper_analyze_group(const Analysis& A, const std::vector<int>& stage
   return o.str();
 }
 
+std::vector<std::vector<int>> merge_candidates(const Analysis& A, const Schedule& sch) {
+  std::vector<std::vector<int>> out{sch.group_of_stage};
+  const int ng = (int)sch.groups.size();
+  for (int gi = 0; gi + 1 < ng; ++gi) {
+    std::vector<int> merged = sch.groups[gi].stages;
+    merged.insert(merged.end(), sch.groups[gi + 1].stages.begin(), sch.groups[gi + 1].stages.end());
+    if (!feasible_stage_set(A, merged)) continue;
+    std::vector<int> gos = sch.group_of_stage;
+    for (int& v : gos)
+      if (v == gi + 1) v = gi;
+      else if (v > gi + 1) --v;
+    out.push_back(gos);
+  }
+  return out;
+}
+
 }  // namespace pmg

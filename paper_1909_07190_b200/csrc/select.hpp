@@ -48,6 +48,10 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
 Schedule schedule(const Analysis& A, const pmg_gpu_spec& spec, const pmg_weights& w, const pmg_sched_opts& opts,
                   const RegProbe* probe = nullptr);
 
+// group_of_stage vectors for measured selection (pmg_sched_opts.tune): the schedule's own grouping, then every
+// grouping that merges two neighbouring groups of it into one feasible stage set
+std::vector<std::vector<int>> merge_candidates(const Analysis& A, const Schedule& sch);
+
 // the paper's §4 geometry + Alg. 2 for an explicit group and (T, B, fracReg, txSz) — analysis pins
 std::string paper_analyze_group(const Analysis& A, const std::vector<int>& stages, const int T[3], const int B[3],
                                 double frac_reg, int tx_size, int regs_per_stage, const pmg_gpu_spec& spec,

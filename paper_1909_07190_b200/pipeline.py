@@ -42,7 +42,7 @@ def weights(name: str = "b200") -> B.Weights:
 
 
 def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, warps=-1, prefetch=-1, tx_size=-1,
-               budget=0, fuse=True, regcap=0, probe=True, cost_model=0, bands=0, inline=True) -> B.SchedOpts:
+               budget=0, fuse=True, regcap=0, probe=True, cost_model=0, bands=0, inline=True, tune=False) -> B.SchedOpts:
     o = B.SchedOpts()
     B.lib.pmg_sched_opts_default(C.byref(o))
     o.vec, o.chunks, o.smem_chunks, o.rows, o.warps, o.prefetch, o.tx_size = (
@@ -54,6 +54,7 @@ def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, 
     o.cost_model = cost_model          # 0: B200 time estimate, 1: Alg. 2 weighted sum
     o.bands = bands                    # expected row-band split (the estimate counts one band's tiles)
     o.no_inline = 0 if inline else 1   # substitute data-expanding stages into their readers
+    o.tune = 1 if tune else 0          # measured selection among the DP schedule and its neighbour merges
     if group_of_stage is not None:
         arr = (C.c_int32 * len(group_of_stage))(*group_of_stage)
         o._keep = arr                      # keep the array alive with the struct

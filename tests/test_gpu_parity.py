@@ -168,3 +168,20 @@ def test_scaled_streams_on_pipelines(name, monkeypatch):
         assert neq == 0
     assert any(s.get("scale", [0, 0, 0]) != [0, 0, 0] for g in plan.describe()["schedule"]["groups"]
                for s in g["config"]["streams"])
+
+
+@pytest.mark.parametrize("name", ["camera", "pyramid_blend"])
+def test_measured_selection(name):
+    """pmg_sched_opts.tune: the DP schedule and each neighbour merge are compiled and timed on the device; the
+    kept plan is the fastest candidate and computes the same function (bit-exact)."""
+    w = PI.small(name, 300, 200) if name == "camera" else PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 160, "H": 96}, 1006)
+    inp = w.inputs() if name == "camera" else w.inputs("structured")
+    exp = evaluate(w.text, w.params, inp)
+    got, plan = run_gpu(w.text, w.params, inp, opts=pmg.sched_opts(tune=True))
+    for k in exp:
+        neq, _ = compare(got[k], exp[k], float_tol=1e-4)
+        assert neq == 0
+    t = plan.describe()["tune"]
+    assert len(t["candidates"]) >= 2
+    us = [c["us"] for c in t["candidates"]]
+    assert us[t["chosen"]] == min(us)
