@@ -229,32 +229,39 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     pmg_sched_opts o0 = *opts;
     o0.tune = 0;
     std::unique_ptr<Plan> best = plan_create(p, params, device, spec, w, &o0);
-    std::vector<std::vector<int>> cands;
-    {
-      CtxGuard g(best->ctx);
-      cands = merge_candidates(best->A, best->sch);
-      double tb = time_plan_us(*best);
-      std::ostringstream js;
-      js << "{\"candidates\":[{\"groups\":" << best->sch.groups.size() << ",\"us\":" << tb << "}";
-      int chosen = 0, pos = 0;
+    // greedy: each round times every neighbour merge of the current best schedule and moves to the fastest,
+    // until no merge helps (at most 4 rounds)
+    CtxGuard g(best->ctx);
+    double tb = time_plan_us(*best);
+    std::ostringstream js;
+    js << "{\"candidates\":[{\"round\":0,\"groups\":" << best->sch.groups.size() << ",\"us\":" << tb << "}";
+    int chosen = 0, pos = 0;
+    std::vector<std::vector<int>> keep;   // group_of_stage arrays must outlive the plans built from them
+    for (int round = 1; round <= 4; ++round) {
+      std::vector<std::vector<int>> cands = merge_candidates(best->A, best->sch);
+      std::unique_ptr<Plan> rbest;
+      double rt = tb;
       for (size_t c = 1; c < cands.size(); ++c) {
+        keep.push_back(cands[c]);
         pmg_sched_opts oc = o0;
-        oc.group_of_stage = cands[c].data();
+        oc.group_of_stage = keep.back().data();
         std::unique_ptr<Plan> Q;
         try {
           Q = plan_create(p, params, device, spec, w, &oc);
         } catch (const Error&) {
           continue;   // a merge the geometry cannot build (e.g. a non-constant dependence)
         }
-        CtxGuard gq(Q->ctx);
         double t = time_plan_us(*Q);
-        js << ",{\"groups\":" << Q->sch.groups.size() << ",\"us\":" << t << "}";
+        js << ",{\"round\":" << round << ",\"groups\":" << Q->sch.groups.size() << ",\"us\":" << t << "}";
         ++pos;
-        if (t < tb) { tb = t; best = std::move(Q); chosen = pos; }
+        if (t < rt) { rt = t; rbest = std::move(Q); chosen = pos; }
       }
-      js << "],\"chosen\":" << chosen << "}";
-      best->tune_json = js.str();
+      if (!rbest) break;
+      tb = rt;
+      best = std::move(rbest);
     }
+    js << "],\"chosen\":" << chosen << "}";
+    best->tune_json = js.str();
     return best;
   }
   auto P = std::make_unique<Plan>();

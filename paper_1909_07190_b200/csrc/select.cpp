@@ -744,13 +744,17 @@ std::string paper_analyze_group(const Analysis& A, const std::vector<int>& stage
 }
 
 std::vector<std::vector<int>> merge_candidates(const Analysis& A, const Schedule& sch) {
-  std::vector<std::vector<int>> out{sch.group_of_stage};
+  // group ids by position in sch.groups (a manual schedule's ids may be any labels)
+  std::vector<int> pos(A.p->stages.size(), 0);
+  for (size_t gi = 0; gi < sch.groups.size(); ++gi)
+    for (int st : sch.groups[gi].stages) pos[st] = (int)gi;
+  std::vector<std::vector<int>> out{pos};
   const int ng = (int)sch.groups.size();
   for (int gi = 0; gi + 1 < ng; ++gi) {
     std::vector<int> merged = sch.groups[gi].stages;
     merged.insert(merged.end(), sch.groups[gi + 1].stages.begin(), sch.groups[gi + 1].stages.end());
     if (!feasible_stage_set(A, merged)) continue;
-    std::vector<int> gos = sch.group_of_stage;
+    std::vector<int> gos = pos;
     for (int& v : gos)
       if (v == gi + 1) v = gi;
       else if (v > gi + 1) --v;

@@ -170,18 +170,21 @@ def test_scaled_streams_on_pipelines(name, monkeypatch):
                for s in g["config"]["streams"])
 
 
-@pytest.mark.parametrize("name", ["camera", "pyramid_blend"])
-def test_measured_selection(name):
-    """pmg_sched_opts.tune: the DP schedule and each neighbour merge are compiled and timed on the device; the
-    kept plan is the fastest candidate and computes the same function (bit-exact)."""
-    w = PI.small(name, 300, 200) if name == "camera" else PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 160, "H": 96}, 1006)
-    inp = w.inputs() if name == "camera" else w.inputs("structured")
+@pytest.mark.parametrize("name,fuse", [("camera", True), ("pyramid_blend", True), ("unsharp", False), ("harris", False)])
+def test_measured_selection(name, fuse):
+    """pmg_sched_opts.tune: the DP schedule and (greedily, round by round) each neighbour merge are compiled and
+    timed on the device; the kept plan is the fastest candidate and computes the same function (bit-exact).
+    Unfused starting points (one stage per group) make the merge rounds non-trivial."""
+    w = (PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 160, "H": 96}, 1006) if name == "pyramid_blend"
+         else PI.small(name, 300, 200))
+    inp = w.inputs("structured") if name == "pyramid_blend" else w.inputs()
     exp = evaluate(w.text, w.params, inp)
-    got, plan = run_gpu(w.text, w.params, inp, opts=pmg.sched_opts(tune=True))
+    got, plan = run_gpu(w.text, w.params, inp, opts=pmg.sched_opts(tune=True, fuse=fuse))
     for k in exp:
-        neq, _ = compare(got[k], exp[k], float_tol=1e-4)
+        neq, _ = compare(got[k], exp[k], **TOL[name])
         assert neq == 0
     t = plan.describe()["tune"]
-    assert len(t["candidates"]) >= 2
     us = [c["us"] for c in t["candidates"]]
     assert us[t["chosen"]] == min(us)
+    if not fuse:
+        assert len(us) >= 2 and len(plan.describe()["schedule"]["groups"]) < len(plan.pipeline.stages)
