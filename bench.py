@@ -147,6 +147,9 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=8, help="row chunks pipelined by pmg_run_host in the e2e leg")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every run from the host instead of replaying captured CUDA graphs")
+    ap.add_argument("--graph", action="store_true",
+                    help="always replay captured CUDA graphs (default: the faster of graph replay and host launches,"
+                         " measured during warm-up)")
     ap.add_argument("--opts", default="", help="manual schedule, e.g. vec=4,chunks=1,rows=32,warps=4,prefetch=4")
     args = ap.parse_args()
     wl = PI.WORKLOADS[args.workload]
@@ -221,8 +224,10 @@ def main():
             graphs.append(g)
         torch.cuda.synchronize()
 
+    use_graph = bool(graphs)
+
     def step(i):
-        if graphs:
+        if use_graph:
             graphs[i % sets].replay()
         else:
             launch(i, stream)
@@ -230,6 +235,27 @@ def main():
     for i in range(max(3, args.warmup)):
         step(i)
     torch.cuda.synchronize()
+    launch_mode = {}
+    if graphs and not args.graph:
+        # launch strategy only (same kernels, same work): graph replay saves the host path for small bands, but
+        # a graph launch costs a few microseconds of its own; keep the faster on this device (warm-up, untimed)
+        for mode in (True, False):
+            use_graph = mode
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(8):
+                step(i)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            launch_mode[mode] = e0.elapsed_time(e1) / 8
+        use_graph = launch_mode[True] <= launch_mode[False]
+        if world > 1:   # every rank uses the same strategy
+            t = torch.tensor([1.0 if use_graph else 0.0], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            use_graph = bool(t.item() > 0.5)
+        for i in range(3):
+            step(i)
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -310,7 +336,9 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded U[0,1) image, pmg_inputs.py)",
         "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
-                   "launch": "CUDA graph replay per buffer set" if graphs else "host launches",
+                   "launch": ("CUDA graph replay per buffer set" if use_graph else "host launches") +
+                             (" (faster in warm-up: graph %.4f / host %.4f ms)" % (launch_mode[True], launch_mode[False])
+                              if launch_mode else ""),
                    "l2": f"{sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (>= 2x the {l2 / 1e6:.0f} MB L2)",
                    "schedule": [g["config"] for g in desc["schedule"]["groups"]],
                    "kernels": desc["kernels"]},
