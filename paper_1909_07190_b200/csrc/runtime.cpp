@@ -260,6 +260,34 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
       tb = rt;
       best = std::move(rbest);
     }
+    // single-group plans: the model's tile choice is also checked against a small grid of 128-column warp
+    // tiles (V x TX in {1x4, 2x2, 4x1}) and tile heights (unsharp 2048^2: the model picks within 6 % of the
+    // best measured configuration, profiles/unsharp_grid_r01n.txt)
+    if (best->sch.groups.size() == 1) {
+      std::vector<int> one(best->A.p->stages.size(), 0);
+      const int vx[3][2] = {{1, 4}, {2, 2}, {4, 1}};
+      std::unique_ptr<Plan> cbest;
+      double ct = tb;
+      for (auto& q : vx)
+        for (int th : {16, 24, 32, 48, 64, 96}) {
+          pmg_sched_opts oc = o0;
+          oc.group_of_stage = one.data();
+          oc.vec = q[0];
+          oc.chunks = q[1];
+          oc.rows = th;
+          std::unique_ptr<Plan> Q;
+          try {
+            Q = plan_create(p, params, device, spec, w, &oc);
+          } catch (const Error&) {
+            continue;
+          }
+          double t = time_plan_us(*Q);
+          js << ",{\"round\":\"config\",\"V\":" << q[0] << ",\"TX\":" << q[1] << ",\"TH\":" << th << ",\"us\":" << t << "}";
+          ++pos;
+          if (t < ct) { ct = t; cbest = std::move(Q); chosen = pos; }
+        }
+      if (cbest) { tb = ct; best = std::move(cbest); }
+    }
     js << "],\"chosen\":" << chosen << "}";
     best->tune_json = js.str();
     return best;
