@@ -20,8 +20,10 @@ Readings of points where the paper is silent (DESIGN.md §"Readings", SURVEY §8
   R1  reads clamp each index to the producer's domain after the index expression is evaluated;
   R3  f32 arithmetic exactly as written, left to right, round-to-nearest per operation, no contraction;
       IEEE '/' and sqrt; float literals are f32(f64(decimal text));
-  R4  int32 arithmetic (wraps), '/' floors, '%' is non-negative for positive divisors, '>>' arithmetic,
-      f32 -> int truncates toward zero, narrowing conversions wrap;
+  R4  int32 arithmetic (wraps, two's complement); '/' floors and '%' takes the divisor's sign
+      (a == (a/b)*b + a%b); x/0 == 0 and x%0 == 0; a shift count is clamped to [0, 32] first, so
+      a<<c == a*2^c mod 2^32 and a>>c == floor(a/2^c) for every int32 count; f32 -> int truncates toward
+      zero, saturates to [-2^31, 2^31-1] and maps NaN to 0; narrowing conversions wrap;
   R5  min(a,b) = b<a ? b : a, max(a,b) = b>a ? b : a, lerp(a,b,w) = a*(1-w) + b*w, select is exact.
 
 Evaluation is whole-domain per stage with numpy (vectorised, no blocking, fusion or reordering of any
@@ -522,7 +524,10 @@ class Evaluator:
     def _to_int(self, v):
         if v.k == "i":
             return np.asarray(v.a, dtype=np.int32)
-        return np.trunc(np.asarray(v.a)).astype(np.int64).astype(np.int32)  # truncate toward zero (R4)
+        # truncate toward zero, saturate to the int32 range, NaN -> 0 (R4)
+        t = np.trunc(np.asarray(v.a, dtype=np.float64))
+        t = np.where(np.isnan(t), 0.0, np.clip(t, -2147483648.0, 2147483647.0))
+        return t.astype(np.int64).astype(np.int32)
 
     def _to_float(self, v):
         if v.k == "f":
@@ -591,22 +596,24 @@ class Evaluator:
             elif op == "*":
                 r = x * y
             elif op == "/":
-                if k == "i":
-                    if np.any(y == 0):
-                        raise OracleError("integer division by zero")
-                    r = np.floor_divide(x, y)
+                if k == "i":                          # floor division in int64, wrapped to int32; x/0 = 0 (R4)
+                    x64, y64 = np.asarray(x, dtype=np.int64), np.asarray(y, dtype=np.int64)
+                    r = np.where(y64 == 0, 0, np.floor_divide(x64, np.where(y64 == 0, 1, y64)))
+                    r = r.astype(np.int32)
                 else:
                     r = x / y
             elif op == "%":
                 if k != "i":
                     raise OracleError("'%' needs integer operands")
-                if np.any(y == 0):
-                    raise OracleError("integer modulo by zero")
-                r = np.mod(x, y)
+                x64, y64 = np.asarray(x, dtype=np.int64), np.asarray(y, dtype=np.int64)
+                r = np.where(y64 == 0, 0, np.mod(x64, np.where(y64 == 0, 1, y64))).astype(np.int32)  # x%0 = 0
             elif op in ("<<", ">>"):
                 if k != "i":
                     raise OracleError(f"'{op}' needs integer operands")
-                r = np.left_shift(x, y) if op == "<<" else np.right_shift(x, y)
+                c = np.clip(np.asarray(y, dtype=np.int64), 0, 32)      # count clamped to [0, 32] (R4)
+                x64 = np.asarray(x, dtype=np.int64)
+                r = ((x64 << c) & 0xFFFFFFFF) if op == "<<" else (x64 >> c)
+                r = r.astype(np.uint32).view(np.int32) if op == "<<" else r.astype(np.int32)
             elif op in ("<", "<=", ">", ">=", "==", "!="):
                 r = {"<": np.less, "<=": np.less_equal, ">": np.greater, ">=": np.greater_equal,
                      "==": np.equal, "!=": np.not_equal}[op](x, y).astype(np.int32)

@@ -340,12 +340,14 @@ struct Emitter {
     DType dt = r.src_is_stage ? p.stages[r.src].dtype : p.images[r.src].dtype;
     int pnd = (int)e.args.size();
     std::string idx[3] = {"0", "0", "0"};
+    std::string t = "a.t[" + std::to_string(gr.idx) + "]";
     for (int i = 0; i < pnd; ++i) {
       int d = i + 3 - pnd;
       R v = toi(ex(*e.args[i], c));
-      idx[d] = "pmg_clampi(" + v.s + ", 0, " + std::to_string(se.e[d] - 1) + ")";
+      // rows: the buffer's rows (the image for full runs, reading R1; the band's rows for band runs)
+      idx[d] = d == 1 ? "pmg_clampi(" + v.s + ", " + t + ".row_base, " + t + ".row_base + " + t + ".nrows - 1)"
+                      : "pmg_clampi(" + v.s + ", 0, " + std::to_string(se.e[d] - 1) + ")";
     }
-    std::string t = "a.t[" + std::to_string(gr.idx) + "]";
     std::string base = "(" + t + ".ptr + (i64)fr * " + t + ".frame_stride + (i64)(" + idx[0] + ") * " + t + ".plane_pitch + (i64)((" + idx[1] + ") - " + t +
                        ".row_base) * " + t + ".row_pitch)";
     return {"pmg_ldg<" + std::string(ctype(dt)) + ">(" + base + ", " + idx[2] + ")", dtype_is_float(dt) ? Kind::Float : Kind::Int};
@@ -923,13 +925,16 @@ struct Emitter {
     return r;
   }
 
-  // producer row of stream j at virtual row R (clamped to the producer's rows, reading R1)
+  // producer row of stream j at virtual row R, clamped to the rows the producer's buffer holds: the whole
+  // image [0, H) for full runs (reading R1), the band's rows [row_base, row_base + nrows) for band runs --
+  // rows outside a band only feed outputs outside it, and no copy may leave the caller's buffer
   std::string prow(int j, const std::string& R) const {
     const GStream& S = g.streams[j];
-    std::string Hp = "a.t[" + std::to_string(S.tensor_slot) + "].H - 1";
-    if (S.sy == 1) return "pmg_clampi(2 * (" + R + ") + " + std::to_string(S.py) + ", 0, " + Hp + ")";
-    if (S.sy == 2) return "pmg_clampi((" + R + ") >> 1, 0, " + Hp + ")";
-    return "pmg_clampi(" + R + ", 0, H - 1)";
+    std::string T = "a.t[" + std::to_string(S.tensor_slot) + "]";
+    std::string lo = T + ".row_base", hi = T + ".row_base + " + T + ".nrows - 1";
+    if (S.sy == 1) return "pmg_clampi(2 * (" + R + ") + " + std::to_string(S.py) + ", " + lo + ", " + hi + ")";
+    if (S.sy == 2) return "pmg_clampi((" + R + ") >> 1, " + lo + ", " + hi + ")";
+    return "pmg_clampi(" + R + ", " + lo + ", " + hi + ")";
   }
   // producer column of consumer column `c` (the chunk origin) for the x form of stream j
   static std::string pcol(const GStream& S, const std::string& c) {

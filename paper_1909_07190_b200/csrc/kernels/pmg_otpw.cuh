@@ -49,6 +49,7 @@ __device__ __forceinline__ float2 pmg_bc2(float c) { return make_float2(c, c); }
 __device__ __forceinline__ float pmg_fmin(float a, float b) { return (b < a) ? b : a; }
 __device__ __forceinline__ float pmg_fmax(float a, float b) { return (b > a) ? b : a; }
 __device__ __forceinline__ float pmg_i2f(int a) { return __int2float_rn(a); }
+// truncate toward zero; cvt.rzi.s32.f32 saturates out-of-range values and maps NaN to 0 (reading R4)
 __device__ __forceinline__ int pmg_f2i(float a) { return __float2int_rz(a); }
 
 // ------------------------------------------------------------------ int32 semantics (reading R4)
@@ -56,13 +57,21 @@ __device__ __forceinline__ int pmg_iadd(int a, int b) { return (int)((u32)a + (u
 __device__ __forceinline__ int pmg_isub(int a, int b) { return (int)((u32)a - (u32)b); }
 __device__ __forceinline__ int pmg_imul(int a, int b) { return (int)((u32)a * (u32)b); }
 __device__ __forceinline__ int pmg_ineg(int a) { return (int)(0u - (u32)a); }
-__device__ __forceinline__ int pmg_idiv(int a, int b) {      // floor division
+// floor division / divisor-signed remainder (reading R4): x/0 == 0, x%0 == 0, INT_MIN/-1 wraps to INT_MIN
+__device__ __forceinline__ int pmg_idiv(int a, int b) {
+  if (b == 0) return 0;
+  if (b == -1) return pmg_ineg(a);
   int q = a / b;
   return (((a % b) != 0) && ((a < 0) != (b < 0))) ? q - 1 : q;
 }
-__device__ __forceinline__ int pmg_imod(int a, int b) { int r = a % b; return (r != 0 && ((r < 0) != (b < 0))) ? r + b : r; }
-__device__ __forceinline__ int pmg_ishl(int a, int b) { return (int)((u32)a << (b & 31)); }
-__device__ __forceinline__ int pmg_ishr(int a, int b) { return a >> (b & 31); }
+__device__ __forceinline__ int pmg_imod(int a, int b) {
+  if (b == 0 || b == -1) return 0;
+  int r = a % b;
+  return (r != 0 && ((r < 0) != (b < 0))) ? r + b : r;
+}
+// shift counts are clamped to [0, 32] (reading R4): a<<c = a*2^c mod 2^32, a>>c = floor(a/2^c)
+__device__ __forceinline__ int pmg_ishl(int a, int b) { return b <= 0 ? a : (b >= 32 ? 0 : (int)((u32)a << b)); }
+__device__ __forceinline__ int pmg_ishr(int a, int b) { return b <= 0 ? a : a >> (b >= 31 ? 31 : b); }
 __device__ __forceinline__ int pmg_iabs(int a) { return a < 0 ? pmg_ineg(a) : a; }
 __device__ __forceinline__ int pmg_imin(int a, int b) { return (b < a) ? b : a; }
 __device__ __forceinline__ int pmg_imax(int a, int b) { return (b > a) ? b : a; }

@@ -169,3 +169,8 @@ WORKLOADS = {
 def small(name: str, W: int, H: int) -> Workload:
     w = WORKLOADS[name]
     return Workload(w.name, w.pipeline, {"W": W, "H": H}, w.seed, w.note + f" (reduced to {W}x{H})")
+
+
+def blur_frames(n: int, seed: int = 1001) -> np.ndarray:
+    """C1 as a batch: n independent 128x128 f32 frames, U[0,1), frame-major [n][y][x]."""
+    return uniform((n, 128, 128), seed)

@@ -1,14 +1,21 @@
-"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (automatic schedule,
-whole image, one pipeline run on the caller's stream), checked on sampled outputs that the demand-driven
-oracle (oracle/points.py) computes one by one: random interior points plus every corner and the middle of
-every edge (the border-tile kernel's territory).  Bar: bit-exact for integer outputs, and for float outputs
-too by construction (reading R3); the BASELINE tolerance is asserted as the ceiling."""
+"""GPU parity at BASELINE.json's full sizes, WHOLE IMAGES, element by element, in the launch configurations
+bench.py times:
+
+* C2 Harris 6400², C3 unsharp 2048²×3, C4 camera 2528×1920, C5 local Laplacian 2560×1536×3 and Pyramid Blend
+  3840×2160×3 — automatic schedule, whole image, one run on the caller's stream (bench.py N=1);
+* row bands (bench.py N>1, schedule for one band) — every band of N = 8 (Harris, local Laplacian) and N = 4
+  (camera) run separately, stitched, compared with the whole-image oracle;
+* C1 blur 128² as the 4096-frame batch (pmg_run_batch) of bench.py's per-config line.
+
+The oracle is the whole-domain evaluator (oracle/pmg_oracle.py), each workload evaluated once per session.
+Bar: bit-exact for every output, integer and float (reading R3 makes float results identical by
+construction); the BASELINE tolerance is asserted as the ceiling as well."""
 import numpy as np
 import pytest
 
 import pmg_inputs as PI
 from gpu_util import compare, to_device, to_numpy
-from oracle import evaluate_points
+from oracle import evaluate, parse
 
 pytestmark = pytest.mark.gpu
 
@@ -16,55 +23,76 @@ import paper_1909_07190_b200 as pmg  # noqa: E402
 
 TOL = {"blur": dict(float_tol=1e-4), "unsharp": dict(float_tol=1e-4), "harris": dict(rel_range=1e-5),
        "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4)}
+VARIANT = {"local_laplacian": "structured", "pyramid_blend": "structured"}
+
+_ORACLE = {}
 
 
-def sample_points(shape, n, seed):
-    """n random points, plus the corners, edge midpoints and next-to-corner points of every plane."""
-    rng = np.random.default_rng(seed)
-    H, W = shape[-2], shape[-1]
-    ys = np.array([0, 0, H - 1, H - 1, 0, H - 1, H // 2, H // 2, 1, H - 2])
-    xs = np.array([0, W - 1, 0, W - 1, W // 2, W // 2, 0, W - 1, 1, W - 2])
-    planes = shape[0] if len(shape) == 3 else 1
-    cols = [rng.integers(0, s, size=n) for s in shape]
-    cols[-2] = np.concatenate([cols[-2], np.tile(ys, planes)])
-    cols[-1] = np.concatenate([cols[-1], np.tile(xs, planes)])
-    if len(shape) == 3:
-        cols[0] = np.concatenate([cols[0], np.repeat(np.arange(planes), len(ys))])
-    return tuple(c.astype(np.int64) for c in cols)
+def oracle_full(name):
+    """(inputs, {liveout: oracle output}) of the full-size workload, computed once per session."""
+    if name not in _ORACLE:
+        wl = PI.WORKLOADS[name]
+        inp = wl.inputs(VARIANT.get(name, "uniform"))
+        _ORACLE[name] = (inp, evaluate(wl.text, wl.params, inp))
+    return _ORACLE[name]
 
 
-@pytest.mark.parametrize("name", ["harris", "unsharp", "camera", "blur", "local_laplacian", "pyramid_blend"])
-def test_fullsize_sampled_parity(name):
+def assert_identical(name, got, exp, what=""):
+    neq, d = compare(got, exp, **TOL[name])
+    assert neq == 0, f"{name}{what}: {neq} of {exp.size} outputs differ from the oracle (max {d})"
+
+
+@pytest.mark.parametrize("name", ["harris", "unsharp", "camera", "local_laplacian", "pyramid_blend"])
+def test_fullsize_whole_image_parity(name):
     import torch
     wl = PI.WORKLOADS[name]
-    inp = wl.inputs("structured") if name in ("local_laplacian", "pyramid_blend") else wl.inputs()
+    inp, exp = oracle_full(name)
     plan = pmg.Plan(pmg.Pipeline(wl.text), wl.params)              # automatic schedule, as bench.py
     ins = [to_device(inp[io.name], io.dtype, pitched=not io.is_table) for io in plan.inputs]
     outs = plan.run(ins)
     torch.cuda.synchronize()
-    (io, out), = zip(plan.outputs, outs)
-    got = to_numpy(out)
-    pts = sample_points(got.shape, 24 if name in ("local_laplacian", "pyramid_blend") else 96, seed=11)
-    exp = evaluate_points(wl.text, wl.params, inp, io.name, pts)
-    neq, d = compare(np.ascontiguousarray(got[pts]), exp, **TOL[name])
-    assert neq == 0, f"{name}: {neq} sampled outputs differ from the oracle (max {d})"
+    for io, out in zip(plan.outputs, outs):
+        assert_identical(name, to_numpy(out), exp[io.name])
 
 
-def test_fullsize_band_sampled_parity():
-    """Band 2 of 4 of Harris 6400x6400 (the bench.py --gpus 4 launch configuration of rank 2)."""
+@pytest.mark.parametrize("name,nb", [("harris", 8), ("local_laplacian", 8), ("camera", 4), ("unsharp", 2)])
+def test_fullsize_bands_stitched_parity(name, nb):
+    """Every band of the bench's N-GPU launch configuration (schedule for one band, pmg_run_band on exactly the
+    band's input rows), stitched, equals the whole-image oracle."""
     import torch
-    wl = PI.WORKLOADS["harris"]
-    inp = wl.inputs()
+    wl = PI.WORKLOADS[name]
+    inp, exp = oracle_full(name)
+    plan = pmg.Plan(pmg.Pipeline(wl.text), wl.params, opts=pmg.sched_opts(bands=nb))
+    got = {o.name: np.zeros(o.shape, dtype=exp[o.name].dtype) for o in plan.outputs}
+    ws = plan.workspace()
+    for b in range(nb):
+        o_r0, o_r1, i_r0, i_r1 = plan.band_rows(b, nb)
+        ins = [to_device(inp[io.name] if io.is_table else inp[io.name][..., i_r0:i_r1, :], io.dtype,
+                         pitched=not io.is_table) for io in plan.inputs]
+        outs = [pmg.empty_pitched((*o.shape[:-2], o_r1 - o_r0, o.shape[-1]), o.dtype) for o in plan.outputs]
+        plan.run_band(b, nb, ins, outs, ws)
+        torch.cuda.synchronize()
+        for o, t in zip(plan.outputs, outs):
+            got[o.name][..., o_r0:o_r1, :] = to_numpy(t)
+    for o in plan.outputs:
+        assert_identical(name, got[o.name], exp[o.name], f" ({nb} bands)")
+
+
+def test_fullsize_blur_batch_4096():
+    """C1 as bench.py's per-config line runs it: 4096 frames of 128x128 in one pmg_run_batch call; every frame
+    equals the oracle of that frame."""
+    import torch
+    wl = PI.WORKLOADS["blur"]
+    frames = PI.blur_frames(4096)
     plan = pmg.Plan(pmg.Pipeline(wl.text), wl.params)
-    o_r0, o_r1, i_r0, i_r1 = plan.band_rows(2, 4)
-    ins = [to_device(inp["img"][i_r0:i_r1], "f32")]
-    outs = [pmg.empty_pitched((o_r1 - o_r0, wl.params["W"]), "f32")]
-    plan.run_band(2, 4, ins, outs)
+    (io,) = plan.inputs
+    x = pmg.empty_pitched((frames.shape[0], *io.shape), "f32", "cuda:0")
+    x.copy_(torch.from_numpy(frames).to("cuda:0"))
+    (out,) = plan.alloc_outputs(frames.shape[0])
+    plan.run_batch([x], [out])
     torch.cuda.synchronize()
-    got = to_numpy(outs[0])
-    rng = np.random.default_rng(3)
-    ys = np.concatenate([rng.integers(o_r0, o_r1, size=64), [o_r0, o_r0, o_r1 - 1, o_r1 - 1]])
-    xs = np.concatenate([rng.integers(0, wl.params["W"], size=64), [0, wl.params["W"] - 1, 0, wl.params["W"] - 1]])
-    exp = evaluate_points(wl.text, wl.params, inp, "harris", (ys, xs))
-    neq, d = compare(np.ascontiguousarray(got[ys - o_r0, xs]), exp, **TOL["harris"])
-    assert neq == 0, f"{neq} sampled band outputs differ (max {d})"
+    got = to_numpy(out)
+    prog = parse(wl.text)
+    for f in range(frames.shape[0]):
+        exp = evaluate(prog, wl.params, {"img": frames[f]})["blury"]
+        assert_identical("blur", got[f], exp, f" frame {f}")

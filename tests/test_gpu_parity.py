@@ -188,3 +188,24 @@ def test_measured_selection(name, fuse):
     assert us[t["chosen"]] == min(us)
     if not fuse:
         assert len(us) >= 2 and len(plan.describe()["schedule"]["groups"]) < len(plan.pipeline.stages)
+
+
+@pytest.mark.parametrize("W,H,opts", [(24, 24, None), (77, 53, dict(vec=1, chunks=2, rows=5, warps=2, prefetch=2))])
+def test_operator_table_parity(W, H, opts):
+    """Reading R4 on the device: every operator / builtin / cast of tests/ops_table.py over all pairs of its
+    edge-case values (shift counts outside [0, 31], zero and -1 divisors, INT_MIN, NaN, +-inf, out-of-range
+    floats), bit-exact against the oracle (whose values are pinned by hand in test_oracle.py)."""
+    import ops_table as OT
+    inp = OT.inputs(W, H)
+    with np.errstate(all="ignore"):
+        exp = evaluate(OT.TEXT, {"W": W, "H": H}, inp)
+    got, _ = run_gpu(OT.TEXT, {"W": W, "H": H}, inp, opts=pmg.sched_opts(**opts) if opts else None)
+    bad = []
+    for k in OT.STAGES:
+        g, e = got[k], exp[k]
+        same = np.array_equal(g.view(np.uint32), e.view(np.uint32)) if e.dtype == np.float32 else np.array_equal(g, e)
+        if not same:
+            i = np.argwhere((g.view(np.uint32) != e.view(np.uint32)) if e.dtype == np.float32 else (g != e))[0]
+            bad.append((k, tuple(int(v) for v in i), inp["a"][tuple(i)], inp["b"][tuple(i)], inp["f"][tuple(i)],
+                        g[tuple(i)], e[tuple(i)]))
+    assert not bad, bad

@@ -380,3 +380,32 @@ def test_point_oracle_equals_whole_domain(wl):
     pts = tuple(np.concatenate([rng.integers(0, n, size=40), [0, n - 1, n // 2]]) for n in ref.shape)
     got = evaluate_points(wl.text, wl.params, inp, key, pts)
     np.testing.assert_array_equal(got.view(np.uint8), np.ascontiguousarray(ref[pts]).view(np.uint8))
+
+
+# ----------------------------------------------------------------------------- R4 operator table (hand values)
+def test_integer_and_conversion_semantics_hand_values():
+    """Reading R4: shift counts clamped to [0, 32], floor '/' and divisor-signed '%' with
+    x/0 = x%0 = 0, int32 wrap-around, f32 -> int truncating + saturating with NaN -> 0, wrapping narrowing
+    casts and stores, saturating sat_u8/sat_u16, 0/1 logical operators.  Every expected value in
+    tests/ops_table.PINS is worked by hand from those definitions."""
+    import ops_table as OT
+    W = len(OT.PINS)
+    a = np.array([[p[1] for p in OT.PINS]], dtype=np.int64).astype(np.int32)
+    b = np.array([[p[2] for p in OT.PINS]], dtype=np.int64).astype(np.int32)
+    f = np.array([[p[3] for p in OT.PINS]], dtype=np.float32)
+    with np.errstate(all="ignore"):
+        out = evaluate(OT.TEXT, {"W": W, "H": 1}, {"a": a, "b": b, "f": f})
+    bad = [(p, int(out[p[0]][0, i])) for i, p in enumerate(OT.PINS) if int(out[p[0]][0, i]) != p[4]]
+    assert not bad, bad
+
+
+def test_ops_table_covers_every_operator():
+    """The GPU operator-table parity test (tests/test_gpu_parity.py) exercises every binary operator,
+    unary operator and builtin of the grammar."""
+    import ops_table as OT
+    text = OT.TEXT
+    for op in ["<<", ">>", "/", "%", "||", "&&", "!", "+", "-", "*", "<", "==", ">="]:
+        assert op in text, op
+    for fn in ["abs", "absd", "min", "max", "clamp", "select", "sqrt", "f32", "i32", "i16", "u16", "u8",
+               "sat_u8", "sat_u16"]:
+        assert f"{fn}(" in text, fn
