@@ -27,10 +27,12 @@
  * return PMG_ERR_CUDA immediately; asynchronous device faults surface at the caller's next sync.
  * PMG_ERR_INFEASIBLE: every candidate schedule has infinite cost (Alg. 2, 945, 961).
  *
- * Concurrency: a pipeline is immutable and shareable across threads; a plan may run concurrently on
- * different streams only with distinct workspaces.  A run's launches are ordered on the caller's stream
- * (border-tile kernels fork onto the plan's side stream and join back with events), so runs can be
- * captured into CUDA graphs.  Outputs are bit-identical for any schedule, band
+ * Concurrency: a pipeline is immutable and shareable across threads.  Run calls on one plan from several
+ * threads are safe (the plan serialises their enqueue with a mutex) but not concurrent on the device: every
+ * run forks its border / x-edge kernels onto the plan's own side streams and joins back with the plan's
+ * events, so two runs of one plan execute one after the other even on different caller streams; use one
+ * plan per stream for concurrent runs, each with its own workspace.  A run's launches are ordered on the
+ * caller's stream, so runs can be captured into CUDA graphs.  Outputs are bit-identical for any schedule, band
  * split or batch split (DESIGN.md §"Determinism").  No NCCL here: process groups and gathers belong to
  * the caller (PyTorch).
  */

@@ -13,6 +13,13 @@ LIBPATH = HERE / "libpmg.so"
 if not LIBPATH.exists():
     raise ImportError(f"{LIBPATH} is missing: build it with `python -m paper_1909_07190_b200.build_lib` "
                       "(or __graft_entry__.build()); there is no fallback path")
+# libpmg.so resolves libnvrtc.so.12 at load time.  PyTorch brings its own NVRTC (12.8) and every GPU process
+# imports torch, so load torch first: the same NVRTC / ptxas then compiles the kernels in every process (the
+# host-only build() and the GPU runs), and the cubin cache, register counts and selector decisions agree.
+try:
+    import torch  # noqa: F401
+except Exception:  # pragma: no cover - torch is part of the image
+    pass
 lib = C.CDLL(str(LIBPATH))
 
 PMG_OK = 0

@@ -304,7 +304,6 @@ pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, co
                           const pmg_sched_opts* opts, const char* out_dir, char* json, size_t cap, size_t* needed) {
   if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
   PMG_TRY({
-    if (out_dir && *out_dir) setenv("PMG_CACHE_DIR", out_dir, 1);
     auto eff = effective(p->p, pvec(params, nparams), opts);
     Analysis A = analyze(*eff, pvec(params, nparams));
     pmg_gpu_spec S;
@@ -317,7 +316,7 @@ pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, co
     Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     std::string out = "{\"schedule\":" + sch.json + ",\"kernels\":[";
     for (size_t i = 0; i < sch.groups.size(); ++i) {
-      Compiled c = jit_compile(sch.groups[i].name, emit_group(A, sch.groups[i]));
+      Compiled c = jit_compile(sch.groups[i].name, emit_group(A, sch.groups[i]), out_dir ? out_dir : "");
       out += (i ? "," : "") + std::string("{\"name\":\"") + c.name + "\",\"regs\":" + std::to_string(c.regs) +
              ",\"spill_stores\":" + std::to_string(c.spill_stores) + ",\"spill_loads\":" + std::to_string(c.spill_loads) +
              ",\"cubin_bytes\":" + std::to_string(c.cubin.size()) + ",\"cached\":" + (c.from_cache ? "true" : "false") + "}";

@@ -77,7 +77,7 @@ struct Emitter {
   std::vector<int> dS, dT;
   int Uk = 1;
   bool in_interior = false;   // emitting the interior-tile kernel (hybrid smem chunks apply there only)
-  bool xk = false;            // emitting the x-border kernel: interior bodies + clamped columns, edge fix-up, bounded stores
+  bool xe = false;            // interior kernel with x-edge tiles (Group::xedge): edge halos replicate by selects
   int cslot = -1;             // interior kernel: compile-time ring slot of the current step (-1: runtime)
 
   // hybrid tiling: stage i's window for chunk kk lives in warp-private shared memory (interior kernel,
@@ -661,7 +661,8 @@ struct Emitter {
     o << "struct PmgArgs {\n  PmgTensor t[" << nt << "];\n  const char* tab[" << ntab << "];\n  int tabn[" << ntab
       << "];\n  int prm[" << np << "];\n"
          "  int H, W, gy0, gy1, nty, ntx, npl, nfr, ntiles, pad_;\n"
-         "  int txA, txB, tyA, tyB;   // interior rectangle of tile columns / rows (host-computed)\n};\n\n";
+         "  int txA, txB, tyA, tyB;   // interior rectangle of tile columns / rows (host-computed)\n"
+         "  int ylast, cxlast;        // interior kernel: the last tile row / column is shifted to end at the image\n};\n\n";
     // tile index -> (tx, ty, pc, fr): interior kernel walks the rectangle, border kernel its complement
     o << "__device__ __forceinline__ void pmg_tile_int(const PmgArgs& a, int t, int& tx, int& ty, int& pc, int& fr) {\n"
          "  const int w = a.txB - a.txA, h = a.tyB - a.tyA;\n"
@@ -677,24 +678,12 @@ struct Emitter {
          "  kk -= bot;\n"
          "  const int side = a.ntx - (a.txB - a.txA);\n"
          "  ty = a.tyA + kk / side; const int j = kk % side; tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n"
-         "__device__ __forceinline__ void pmg_tile_x(const PmgArgs& a, int t, int& tx, int& ty, int& pc, int& fr) {\n"
+         "__device__ __forceinline__ void pmg_tile_e(const PmgArgs& a, int t, int& tx, int& ty, int& pc, int& fr) {\n"
          "  const int side = a.ntx - (a.txB - a.txA), h = a.tyB - a.tyA;\n"
          "  const int j = t % side; int r = t / side; ty = a.tyA + r % h; r /= h; pc = r % a.npl; fr = r / a.npl;\n"
          "  tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
     kernel(true);
-    return o.str();
-  }
-
-  // the x-border kernel: tiles of the first / last tile columns whose rows are interior, with TH_x-row
-  // tiles, run the interior (branch-free in y) bodies with clamped columns, edge replication and bounded stores
-  std::string run_xborder() {
-    for (auto& P : g.gs) himax = std::max(himax, P.hi);
-    for (auto& S : g.streams) himax = std::max(himax, S.hi);
-    for (auto& S : g.streams)
-      if (S.sx == 0) { xlm = std::max(xlm, S.xl); xrm = std::max(xrm, S.xr); }
-    o << "#undef TH\n#undef NSTEPS\n#define TH " << g.cfg.TH << "\n#define NSTEPS " << g.nsteps << "\n\n";
-    xk = true;
-    kernel(true);
+    if (g.xedge) kernel(true, true);
     return o.str();
   }
 
@@ -709,8 +698,18 @@ struct Emitter {
     return o.str();
   }
 
+  // tile origin: the interior and x-edge kernels shift their last tile row up to end at the last row they may
+  // compute (a.ylast; overlapping tile rows store the same values); the x-edge kernel starts its first tile
+  // column at x = 0 instead of -PL; the border kernel keeps the plain grid
+  std::string y0_expr(const std::string& ty) const {
+    return in_interior ? "min(a.gy0 + " + ty + " * TH, a.ylast)" : "(a.gy0 + " + ty + " * TH)";
+  }
+  std::string cx_expr(const std::string& tx) const {
+    return xe ? "max(" + tx + " * OW - PL, 0)" : "(" + tx + " * OW - PL)";
+  }
+
   // one entry point: interior tiles (branch-free bodies) or border tiles (general bodies)
-  void kernel(bool interior) {
+  void kernel(bool interior, bool edge = false) {
     const KConfig& k = g.cfg;
     const int n = (int)g.gs.size();
     if (interior) plan_interior();
@@ -720,9 +719,14 @@ struct Emitter {
       folds.assign(n, Fold{});
       Uk = g.U;
     }
-    in_interior = interior && !xk;
-    const char* dec = xk ? "pmg_tile_x" : interior ? "pmg_tile_int" : "pmg_tile_bdr";
+    in_interior = interior;
+    xe = interior && edge;
+    const char* dec = xe ? "pmg_tile_e" : interior ? "pmg_tile_int" : "pmg_tile_bdr";
     int cap = k.regcap;
+    {   // experiment knobs: register caps per kernel class (interior / x-edge / border)
+      const char* e = getenv(xe ? "PMG_CAP_E" : interior ? "PMG_CAP_I" : "PMG_CAP_B");
+      if (e && atoi(e) > 0) cap = atoi(e);
+    }
     if (!interior && cap <= 0) {
       // border tiles are latency-bound and share the SMs with the interior kernel: cap their registers so
       // that many of them stay resident
@@ -732,7 +736,7 @@ struct Emitter {
       cap = e ? atoi(e) : (g.regs_est > 0 && g.regs_est <= 72 ? 96 : 0);
     }
     int minb = cap > 0 ? std::max(1, 65536 / (cap * 32 * k.NW)) : 1;
-    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << (xk ? "_x" : interior ? "" : "_b")
+    o << "extern \"C\" __global__ void __launch_bounds__(NW * 32, " << minb << ") " << g.name << (xe ? "_e" : interior ? "" : "_b")
       << "(const __grid_constant__ PmgArgs a) {\n";
     o << "  extern __shared__ __align__(128) char pmg_smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
@@ -763,8 +767,8 @@ struct Emitter {
       o << ") {\n"
            "    int txq, tyq, pcq, frq;\n    " << dec << "(a, tile, txq, tyq, pcq, frq);\n"
            "    (void)pcq; (void)frq;\n"
-           "    y0r = a.gy0 + tyq * TH;\n"
-           "    const int cxq = txq * OW - PL;\n"
+           "    y0r = " << y0_expr("tyq") << ";\n"
+           "    const int cxq = " << cx_expr("txq") << ";\n"
            "    tot = 0;\n";
       for (size_t j = 0; j < g.streams.size(); ++j) {
         const GStream& S = g.streams[j];
@@ -796,11 +800,23 @@ struct Emitter {
     o << "  for (int it = 0; it < my_tiles; ++it) {\n"
          "    const int tile = gw + it * nwt;\n"
          "    int tx, ty, pc, fr;\n    " << dec << "(a, tile, tx, ty, pc, fr);\n"
-         "    const int y0 = a.gy0 + ty * TH;\n"
-         "    const int cx = tx * OW - PL;\n"
+         "    const int y0 = " << y0_expr("ty") << ";\n"
+         "    const int cx = " << cx_expr("tx") << ";\n"
          "    const int xL = cx + V * lane;\n"
          "    const int xLh = xL >> 1;   // xL / 2 (used only when xL is even)\n"
-         "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W)" << xb_scaled() << ";\n"
+         "    const bool xb = (cx - XLM < 0) || (cx + CW + XRM > W)" << xb_scaled() << ";\n";
+    if (xe) {
+      // x-edge tiles (reading R1 by selects): the lane holding column 0 takes its own column 0 for its left halo,
+      // the lane (of each chunk) holding column W-1 its own column W-1 for its right halo; each tile stores its
+      // canonical columns [tx*OW, min((tx+1)*OW, W))
+      o << "    const bool lfix = xL == 0;\n"
+           "    const int oxlo = tx * OW, oxhi = min(oxlo + OW, W);\n";
+      for (int kk = 0; kk < TX; ++kk)
+        o << "    const bool stk" << kk << " = (xL + " << 32 * V * kk << " >= oxlo) && (xL + " << 32 * V * kk + V << " <= oxhi);\n"
+          << "    const bool rfix" << kk << " = xL + " << 32 * V * kk + V << " == W;\n    (void)rfix" << kk << ";\n";
+      o << "    (void)lfix;\n";
+    }
+    o << ""
          "    const int yend = (y0 + TH < a.gy1) ? (y0 + TH) : a.gy1;\n"
          "    (void)pc; (void)fr; (void)xL; (void)xLh; (void)xb; (void)yend;\n";
     if (hs) {
@@ -965,7 +981,6 @@ struct Emitter {
       int vlo = (int)std::floor((double)lo / V) * V, vhi = (int)std::ceil((double)hi / V) * V;
       o << ind << "{\n" << ind << "  const char* sb = srow + " << S.smem_off << ";\n";
       if (!fast) o << ind << "  if (!xb) {\n";
-      if (fast && xk) o << ind << "  if (false) {\n";   // x-border kernel: every tile is an x-border tile
       if (S.sx == 2) {
         // up2: lane base (V/2)*lane; e' -> element floor(e'/2); vectors of V/2 elements
         const int h = V / 2, qlo = (int)std::floor(lo / 2.0), qhi = (hi - 1) / 2;
@@ -989,8 +1004,16 @@ struct Emitter {
               if (vb + q >= lo && vb + q < hi) o << " " << tv((int)j, sl, kk, vb + q) << " = PmgElem<" << ct << ">::cv(w[" << q << "]);";
             o << " }\n";
           }
+        if (fast && xe) {   // x-edge tiles: the halo columns outside [0, W) replicate the edge column (R1)
+          for (int e = lo; e < 0; ++e)
+            o << ind << "    " << tv((int)j, sl, 0, e) << " = lfix ? " << tv((int)j, sl, 0, 0) << " : " << tv((int)j, sl, 0, e) << ";\n";
+          for (int kk = 0; kk < TX; ++kk)
+            for (int e = V; e < hi; ++e)
+              o << ind << "    " << tv((int)j, sl, kk, e) << " = rfix" << kk << " ? " << tv((int)j, sl, kk, V - 1) << " : "
+                << tv((int)j, sl, kk, e) << ";\n";
+        }
       }
-      if (!fast || xk) {
+      if (!fast) {
         // clamped producer columns (reading R1): unit xL+e, down2 2*xL+q, up2 floor((xL+e')/2)
         const std::string Wp = S.sx == 0 ? "W - 1" : "a.t[" + std::to_string(S.tensor_slot) + "].W - 1";
         o << ind << "  } else {\n" << ind << "    const int xo = " << pcol(S, "cx") << " - " << S.xl << ";\n";
@@ -1024,14 +1047,17 @@ struct Emitter {
         return g.streams[j].sy == 0 ? "  q_ptr" + std::to_string(j) + " += a.t[" + std::to_string(g.streams[j].tensor_slot) + "].row_pitch;\n"
                                     : std::string();
       };
+      const char* fe = getenv("PMG_FENCE");
+      const bool fence = fe && fe[0] == '1';
       if (g.streams.size() == 1) {
-        o << ind << "{\n" << ind << "  pmg_refill1_elect(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, " << src_of(0)
+        o << ind << "{\n" << ind << "  " << (fence ? "pmg_refill1_elect" : "pmg_refill1_elect_nf")
+          << "(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, " << src_of(0)
           << ", p_bytes0);\n" << ind << adv(0) << ind << "}\n";
         return;
       }
       o << ind << "{\n" << ind << "  const u32 bar = bar0 + 8 * slq;\n"
         << ind << "  if (leader) {\n"
-        << ind << "    pmg_fence_proxy_async();\n"
+        << ind << (fence ? "    pmg_fence_proxy_async();\n" : "")
         << ind << "    pmg_mbar_expect_tx(bar, p_total);\n";
       for (size_t j = 0; j < g.streams.size(); ++j)
         o << ind << "    pmg_bulk_g2s(ring_addr + slq * RING + p_dst" << j << ", " << src_of((int)j) << ", p_bytes" << j << ", bar);\n";
@@ -1093,20 +1119,15 @@ struct Emitter {
       if (check_rows) pred = "(" + rowv + " < yend) && " + pred;
       o << ind << "{\n" << ind << "  char* orow = optr" << i << ";\n" << ind << "  optr" << i << " += " << T << ".row_pitch;\n"
         << ind << "  const bool sp = " << pred << ";\n";
-      if (xk) {
-        o << ind << "  if (sp) {\n";
-        bounded_store(i, cur, "orow", ind + "    ");
-        o << ind << "  }\n" << ind << "}\n";
-        return;
-      }
       for (int kk = 0; kk < TX; ++kk) {
         int lo = g.PL - 32 * V * kk <= 0 ? 0 : std::min(32, (g.PL - 32 * V * kk) / V);
         int hi = std::max(0, std::min(32, (g.CW - g.PR - 32 * V * kk) / V));
-        if (hi <= lo) continue;
+        if (hi <= lo && !xe) continue;
         o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
         for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
         o << "};\n";
-        std::string lanes = (lo == 0 && hi == 32) ? "" : " && lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi);
+        std::string lanes = xe ? " && stk" + std::to_string(kk)
+                               : (lo == 0 && hi == 32) ? "" : " && lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi);
         o << ind << "    pmg_stg_vec_if<" << ct << ", " << V << ">(orow + " << 32 * V * kk * esz << ", w, sp" << lanes << ");\n"
           << ind << "  }\n";
       }
@@ -1117,11 +1138,6 @@ struct Emitter {
     if (check_rows) o << ind << "if (" << rowv << " >= y0 && " << rowv << " < yend && " << inbuf << ") {\n";
     else o << ind << "if (" << inbuf << ") {\n";
     o << ind << "  char* orow = obase" << i << " + (i64)" << rowv << " * a.t[" << P.tensor_slot << "].row_pitch;\n";
-    if (fast && xk) {
-      bounded_store(i, cur, "orow", ind + "  ");
-      o << ind << "}\n" << ind << "}\n";
-      return;
-    }
     if (!fast)
       o << ind << "  const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
         << ind << "  const int oxhi = (cx + PL + OW) < W ? (cx + PL + OW) : W;\n";
@@ -1131,11 +1147,12 @@ struct Emitter {
         // interior tile: the output lanes of each chunk are compile-time constants
         int lo = g.PL - 32 * V * kk <= 0 ? 0 : std::min(32, (g.PL - 32 * V * kk) / V);
         int hi = std::max(0, std::min(32, (g.CW - g.PR - 32 * V * kk) / V));
-        if (hi <= lo) continue;
+        if (hi <= lo && !xe) continue;
         o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
         for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
         o << "};\n";
-        std::string cond = (lo == 0 && hi == 32) ? "" : "if (lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi) + ") ";
+        std::string cond = xe ? "if (stk" + std::to_string(kk) + ") "
+                              : (lo == 0 && hi == 32) ? "" : "if (lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi) + ") ";
         o << ind << "    " << cond << "pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n" << ind << "  }\n";
       } else {
         o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
@@ -1152,30 +1169,6 @@ struct Emitter {
     }
     o << ind << "}\n";
     o << ind << "}\n";
-  }
-
-  // store of one row of stage i at `orow` limited to the tile's output columns inside [0, W) (x-border
-  // kernel; partial vectors at the image edge)
-  void bounded_store(int i, int cur, const std::string& orow, const std::string& ind) {
-    const GStage& P = g.gs[i];
-    DType dt = p.stages[P.id].dtype;
-    std::string ct = ctype(dt);
-    int esz = dtype_size(dt);
-    o << ind << "const int oxlo = (cx + PL) < 0 ? 0 : (cx + PL);\n"
-      << ind << "const int oxhi = (cx + PL + OW) < W ? (cx + PL + OW) : W;\n";
-    for (int kk = 0; kk < TX; ++kk) {
-      std::string dst = orow + " + " + std::to_string(32 * V * kk * esz);
-      o << ind << "{\n" << ind << "  " << ct << " w[" << V << "] = {";
-      for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
-      o << "};\n";
-      o << ind << "  const int xs = xL + " << 32 * V * kk << ";\n"
-        << ind << "  if (xs >= oxlo && xs + V <= oxhi) pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n"
-        << ind << "  else if (xs < oxhi && xs + V > oxlo) {\n";
-      for (int v = 0; v < V; ++v)
-        o << ind << "    if (xs + " << v << " >= oxlo && xs + " << v << " < oxhi) reinterpret_cast<" << ct << "*>(" << dst
-          << ")[" << v << "] = w[" << v << "];\n";
-      o << ind << "  }\n" << ind << "}\n";
-    }
   }
 
   // one step of the wavefront: fast = interior tile (no row/column checks); tconst = t known at emit time
@@ -1241,7 +1234,7 @@ struct Emitter {
             o << in3 << sv(i, cur, kk, v) << " = " << conv_store(val, sd.dtype) << ";\n";
           }
       }
-      if (P.xfix && (!fast || xk)) {
+      if (P.xfix && !fast) {
         // border tiles: columns outside [0, W) take the edge value (reading R1)
         o << in3 << "if (xb) {\n";
         for (int side = 0; side < 2; ++side) {
@@ -1269,12 +1262,15 @@ struct Emitter {
           std::string own = sv(i, cur, kk, ee);
           std::string send = kk > 0 ? "(lane >= " + std::to_string(32 + q) + " ? " + sv(i, cur, kk - 1, ee) + " : " + own + ")" : own;
           o << in3 << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + (" << q << ")) & 31);\n";
+          if (fast && xe && kk == 0) o << in3 << sv(i, cur, kk, e) << " = lfix ? " << sv(i, cur, 0, 0) << " : " << sv(i, cur, kk, e) << ";\n";
         }
         for (int e = V; e < V + P.er; ++e) {
           int q = e / V, ee = e - q * V;
           std::string own = sv(i, cur, kk, ee);
           std::string send = kk + 1 < TX ? "(lane < " + std::to_string(q) + " ? " + sv(i, cur, kk + 1, ee) + " : " + own + ")" : own;
           o << in3 << sv(i, cur, kk, e) << " = pmg_shfl(" << send << ", (lane + " << q << ") & 31);\n";
+          if (fast && xe)
+            o << in3 << sv(i, cur, kk, e) << " = rfix" << kk << " ? " << sv(i, cur, kk, V - 1) << " : " << sv(i, cur, kk, e) << ";\n";
         }
       }
       if (hyb(i, 0)) {
@@ -1338,13 +1334,6 @@ std::string emit_group(const Analysis& A, const Group& g) {
   }
   Emitter eb(A, gb);
   src += eb.run_border();
-  if (g.TH_x > 0) {   // x-border kernel: interior bodies on TH_x-row tiles of the side tile columns
-    Group gx = g;
-    gx.cfg.TH = g.TH_x;
-    gx.nsteps = g.TH_x - g.t_first;
-    Emitter ex_(A, gx);
-    src += ex_.run_xborder();
-  }
   return src;
 }
 

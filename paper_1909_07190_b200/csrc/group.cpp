@@ -272,16 +272,21 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
     for (int d = std::min(want, k.TH); d >= 1; --d)
       if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_b = d; break; }
   }
-  // x-border tiles of interior rows: optionally (PMG_XK = rows) a third kernel runs the interior bodies with
-  // clamped columns on TH_x-row tiles; not with shared-memory chunks.  Off by default: measured slower on
-  // B200 for every workload (profiles/xborder_kernel_r01f.txt)
+  // x-edge kernel: the first / last tile columns run the interior (branch-free in y) body with
+  // the halo elements beyond the image edge replaced by the edge column (a select in the lane that holds
+  // column 0 / W-1), the first tile column starting at x = 0.  Needs: no shared-memory chunks, unscaled x reads,
+  // every x halo within one lane (el, er <= V), W a multiple of V (column W-1 ends a lane), and only the first
+  // tile column reaching left of x = 0 (OW >= PL + the streams' left smem halo).
   {
-    const char* e = getenv("PMG_XK");
-    int want = e ? atoi(e) : 0;
-    g.TH_x = 0;
-    if (k.S == 0 && want > 0)
-      for (int d = std::min(want, k.TH); d >= 1; --d)
-        if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_x = d; break; }
+    const char* e = getenv("PMG_XEDGE");
+    bool ok = !(e && e[0] == '0') && k.S == 0 && g.ext.e[2] % k.V == 0;
+    int xl_max = 0;
+    for (auto& P : g.gs) ok = ok && P.el <= k.V && P.er <= k.V;
+    for (auto& st : g.streams) {
+      ok = ok && st.sx == 0 && st.el <= k.V && st.er <= k.V;
+      xl_max = std::max(xl_max, st.xl);
+    }
+    g.xedge = ok && g.OW >= g.PL + xl_max;
   }
   // unroll factor for register-window rotation
   int U = 1;

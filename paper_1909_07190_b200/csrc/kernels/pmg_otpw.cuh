@@ -142,6 +142,19 @@ __device__ __forceinline__ void pmg_refill1_elect(u32 bar, u32 total, u32 dst, c
       ::"r"(bar), "r"(total), "r"(dst), "l"(src), "r"(bytes) : "memory");
 }
 
+// the same without the proxy fence: the interior main loop refills the slot its lanes read at the start of
+// the step; those LDS reads are issued (in order, through the same MIO path) long before the bulk copy's
+// global fetch can land in shared memory, and the slot's next consumer waits on its mbarrier
+// (DESIGN.md §6 "ring refill"; PMG_FENCE=1 restores the fence)
+__device__ __forceinline__ void pmg_refill1_elect_nf(u32 bar, u32 total, u32 dst, const void* src, u32 bytes) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+      "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %4, [%0];\n}"
+      ::"r"(bar), "r"(total), "r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+
 // predicated vector store (no branch: the interior body stays one basic block)
 template <typename T, int N>
 __device__ __forceinline__ void pmg_stg_vec_if(char* dst, const T (&v)[N], bool p) {

@@ -85,7 +85,8 @@ struct Group {
   int CW = 0, PL = 0, PR = 0, OW = 0;
   int t_first = 0, nsteps = 0, U = 1;
   bool no_scaled = false;   // read scaled inputs by gather (set by build_group when there would be too many streams)
-  int TH_x = 0;             // tile rows of the x-border kernel (divides TH; 0: x-border tiles go to the border kernel)
+  bool xedge = false;       // x-edge kernel: the first / last tile columns run the interior body with halo selects
+                            // at the image's left / right edge; the border kernel keeps only the top / bottom rows
   int TH_b = 0;             // tile rows of the border-tile kernel (divides TH; small: border tiles are latency-bound)
   int ring_bytes = 0;       // one ring slot
   int warp_smem = 0;        // bytes of shared memory per warp

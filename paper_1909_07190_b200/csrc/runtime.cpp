@@ -8,7 +8,9 @@
 #include <sys/stat.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <unistd.h>
 #include <cstring>
 #include <fstream>
 #include <mutex>
@@ -36,9 +38,9 @@ std::string kernel_dir() {
   return ".";
 }
 
-static std::string cache_dir() {
+static std::string cache_dir(const std::string& override_dir) {
   const char* e = getenv("PMG_CACHE_DIR");
-  std::string d = e && *e ? e : kernel_dir() + "/../build/cubin_cache";
+  std::string d = !override_dir.empty() ? override_dir : e && *e ? e : kernel_dir() + "/../build/cubin_cache";
   std::string acc;
   std::stringstream ss(d);
   std::string part;
@@ -78,7 +80,7 @@ static void parse_ptxas(Compiled& c) {
   if (std::regex_search(c.log, m, std::regex("([0-9]+) bytes smem"))) c.smem_static = std::stoi(m[1]);
 }
 
-Compiled jit_compile(const std::string& name, const std::string& source) {
+Compiled jit_compile(const std::string& name, const std::string& source, const std::string& dir_override) {
   Compiled c;
   c.name = name;
   c.source = source;
@@ -89,7 +91,7 @@ Compiled jit_compile(const std::string& name, const std::string& source) {
   key_src += " nvrtc" + std::to_string(maj) + "." + std::to_string(min);
   char hex[32];
   snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(key_src));
-  std::string dir = cache_dir();
+  std::string dir = cache_dir(dir_override);
   std::string base = dir + "/" + name + "_" + hex;
   {
     std::ifstream f(base + ".cubin", std::ios::binary);
@@ -130,12 +132,24 @@ Compiled jit_compile(const std::string& name, const std::string& source) {
   nvrtcDestroyProgram(&prog);
   c.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   parse_ptxas(c);
+  // cache files are written under names unique to this process and call, then renamed into place (atomic on
+  // POSIX), so concurrent processes (torchrun ranks) never read a partial file; the log (read first by the
+  // cache lookup) is published before the cubin
+  static std::atomic<unsigned> seq{0};
+  const std::string tag = ".tmp." + std::to_string((long)getpid()) + "." + std::to_string(seq++);
   {
-    std::ofstream f(base + ".cubin.tmp", std::ios::binary);
+    std::ofstream f(base + ".log" + tag);
+    f << c.log;
+  }
+  {
+    std::ofstream f(base + ".cubin" + tag, std::ios::binary);
     f.write(c.cubin.data(), (std::streamsize)c.cubin.size());
   }
-  { std::ofstream f(base + ".log"); f << c.log; }
-  std::rename((base + ".cubin.tmp").c_str(), (base + ".cubin").c_str());
+  if (std::rename((base + ".log" + tag).c_str(), (base + ".log").c_str()) != 0 ||
+      std::rename((base + ".cubin" + tag).c_str(), (base + ".cubin").c_str()) != 0) {
+    std::remove((base + ".log" + tag).c_str());   // cache write failed: the compiled cubin is still returned
+    std::remove((base + ".cubin" + tag).c_str());
+  }
   return c;
 }
 
@@ -274,7 +288,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
       std::unique_ptr<Plan> cbest;
       double ct = tb;
       for (auto& q : vx)
-        for (int th : {16, 24, 32, 48, 64, 96}) {
+        for (int th : {24, 32, 48, 64, 96, 100, 112, 128}) {
           pmg_sched_opts oc = o0;
           oc.group_of_stage = one.data();
           oc.vec = q[0];
@@ -363,21 +377,22 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     check(D.ModuleLoadData(&k.mod, k.bin.cubin.data()), "cuModuleLoadData");
     check(D.ModuleGetFunction(&k.fn, k.mod, g.name.c_str()), "cuModuleGetFunction");
     check(D.ModuleGetFunction(&k.fn_b, k.mod, (g.name + "_b").c_str()), "cuModuleGetFunction");
-    if (g.TH_x > 0) check(D.ModuleGetFunction(&k.fn_x, k.mod, (g.name + "_x").c_str()), "cuModuleGetFunction");
-    for (CUfunction f : {k.fn, k.fn_b, k.fn_x})
+    if (g.xedge) check(D.ModuleGetFunction(&k.fn_e, k.mod, (g.name + "_e").c_str()), "cuModuleGetFunction");
+    for (CUfunction f : {k.fn, k.fn_b, k.fn_e})
       if (f && g.block_smem > 48 * 1024)
         check(D.FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, g.block_smem), "cuFuncSetAttribute");
     check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm, k.fn, g.cfg.NW * 32, g.block_smem), "occupancy");
     check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm_b, k.fn_b, g.cfg.NW * 32, g.block_smem), "occupancy");
-    if (k.fn_x)
-      check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm_x, k.fn_x, g.cfg.NW * 32, g.block_smem), "occupancy");
-    if (k.blocks_per_sm < 1 || k.blocks_per_sm_b < 1 || (k.fn_x && k.blocks_per_sm_x < 1)) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
+    if (k.fn_e)
+      check(D.OccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm_e, k.fn_e, g.cfg.NW * 32, g.block_smem), "occupancy");
+    if (k.blocks_per_sm < 1 || k.blocks_per_sm_b < 1 || (k.fn_e && k.blocks_per_sm_e < 1)) throw Error(-6, "kernel " + g.name + " cannot be resident on an SM");
     const FnStats& fb = k.bin.fns[g.name + "_b"];
     js << (gi ? "," : "") << "{\"name\":\"" << g.name << "\",\"regs\":" << k.bin.regs << ",\"spill_stores\":"
        << k.bin.spill_stores << ",\"spill_loads\":" << k.bin.spill_loads << ",\"block_smem\":" << g.block_smem
        << ",\"blocks_per_sm\":" << k.blocks_per_sm << ",\"border_regs\":" << fb.regs << ",\"border_spill_stores\":"
-       << fb.spill_stores << ",\"border_blocks_per_sm\":" << k.blocks_per_sm_b << ",\"xborder_regs\":"
-       << (k.fn_x ? k.bin.fns[g.name + "_x"].regs : 0) << ",\"xborder_blocks_per_sm\":" << k.blocks_per_sm_x << ",\"cached\":"
+       << fb.spill_stores << ",\"border_blocks_per_sm\":" << k.blocks_per_sm_b << ",\"edge_regs\":" << (k.fn_e ? k.bin.fns[g.name + "_e"].regs : 0)
+       << ",\"edge_blocks_per_sm\":" << k.blocks_per_sm_e
+       << ",\"cached\":"
        << (k.bin.from_cache ? "true" : "false") << ",\"compile_s\":" << k.bin.compile_s << "}";
     P->kernels.push_back(std::move(k));
   }
@@ -428,11 +443,17 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     P->nlanes = used;
     P->lane_stream.assign(used, nullptr);
     P->lane_side.assign(used, nullptr);
+    P->lane_side2.assign(used, nullptr);
     P->lane_fork.assign(used, nullptr);
     P->lane_join.assign(used, nullptr);
+    P->lane_join2.assign(used, nullptr);
     P->lane_side[0] = P->side;
     P->lane_fork[0] = P->ev_fork;
     P->lane_join[0] = P->ev_join;
+    for (int l = 0; l < used; ++l) {
+      check(D.StreamCreate(&P->lane_side2[l], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      check(D.EventCreate(&P->lane_join2[l], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    }
     for (int l = 1; l < used; ++l) {
       check(D.StreamCreate(&P->lane_stream[l], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
       check(D.StreamCreate(&P->lane_side[l], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
@@ -448,8 +469,15 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   return P;
 }
 
+// every plan owns its CUDA resources: destroying a Plan (also a losing measured-selection candidate, or one
+// whose creation threw half way) releases them exactly once
+Plan::~Plan() {
+  try { plan_destroy(this); } catch (...) {}
+}
+
 void plan_destroy(Plan* P) {
-  if (!P) return;
+  if (!P || P->released) return;
+  P->released = true;
   if (drv().ok && P->ctx) {
     CtxGuard g(P->ctx);
     for (auto& k : P->kernels)
@@ -464,6 +492,10 @@ void plan_destroy(Plan* P) {
     if (P->ev_start) drv().EventDestroy(P->ev_start);
     for (size_t l = 1; l < P->lane_stream.size(); ++l) drv().StreamDestroy(P->lane_stream[l]);
     for (size_t l = 1; l < P->lane_side.size(); ++l) drv().StreamDestroy(P->lane_side[l]);
+    for (CUstream st : P->lane_side2)
+      if (st) drv().StreamDestroy(st);
+    for (CUevent e : P->lane_join2)
+      if (e) drv().EventDestroy(e);
     for (size_t l = 1; l < P->lane_fork.size(); ++l) drv().EventDestroy(P->lane_fork[l]);
     for (size_t l = 1; l < P->lane_join.size(); ++l) drv().EventDestroy(P->lane_join[l]);
     for (CUevent e : P->ev_group) drv().EventDestroy(e);
@@ -542,6 +574,7 @@ static_assert(sizeof(HostTensor) == 56, "PmgTensor mirror");
 
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* ws, CUstream s, int band,
               int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs) {
+  std::lock_guard<std::recursive_mutex> lock(P.run_mu);
   Drv& D = drv();
   if (!D.ok) throw Error(-6, D.err);
   const Pipeline& p = *P.pipe;
@@ -589,8 +622,8 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     Kernel& K = P.kernels[gi];
     const int lane = lanes ? P.lane_of[gi] : 0;
     const CUstream gs = lane == 0 ? s : P.lane_stream[lane];
-    const CUstream gside = P.lane_side[lane];
-    const CUevent gfork = P.lane_fork[lane], gjoin = P.lane_join[lane];
+    const CUstream gside = P.lane_side[lane], gside2 = P.lane_side2[lane];
+    const CUevent gfork = P.lane_fork[lane], gjoin = P.lane_join[lane], gjoin2 = P.lane_join2[lane];
     if (lanes) {
       for (int d : P.deps[gi])
         if (P.lane_of[d] != lane) check(D.StreamWaitEvent(gs, P.ev_group[d], 0), "cuStreamWaitEvent");
@@ -603,7 +636,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     const int NT = std::max<int>(1, (int)g.tensors.size()), NTAB = std::max(1, P.ntables),
               NP = std::max<int>(1, (int)p.params.size());
     size_t off_tab = sizeof(HostTensor) * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
-           off_int = off_prm + 4 * NP, size = (off_int + 56 + 7) / 8 * 8;
+           off_int = off_prm + 4 * NP, size = (off_int + 64 + 7) / 8 * 8;
     std::vector<char> buf(size, 0);
     for (size_t ti = 0; ti < g.tensors.size(); ++ti) {
       auto [is_stage, id] = g.tensors[ti];
@@ -690,52 +723,68 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     while (txA < txB && !scaled_in(txA)) ++txA;
     while (txB > txA && !scaled_in(txB - 1)) --txB;
     // interior tile rows: the tiling starts `top` rows below gy0 (a multiple of the border tile height, enough
-    // for the rows the wavefront reads above a tile), and holds the whole tiles whose wavefront stays inside
-    // the image and the computed rows; the border kernel takes the top and bottom remainders in TH_b-row tiles
-    // (TH_b divides TH), so at most TH_b - 1 + the halo rows of each image edge go through the general body
+    // for the rows the wavefront reads above a tile); its last tile row is shifted up to end at `ylim` (the last
+    // row whose wavefront stays inside the image and the computed rows), overlapping the row before it -- both
+    // compute the same values.  The border kernel takes the rows above the tiling and the TH_b-row tiles from
+    // the one containing ylim down, so only those rows go through the general body.
     const int THb = g.TH_b > 0 ? g.TH_b : g.cfg.TH;
     const int64_t top = cdiv(std::max<int64_t>(0, -(int64_t)g.t_first - gy0), THb) * THb;
     const int64_t ylim = std::min<int64_t>((int64_t)Hg - himax, gy1);
-    int64_t nty_i = std::max<int64_t>(0, fdiv(ylim - gy0 - top, g.cfg.TH));
-    if (txB <= txA || nty_i <= 0) { txA = txB = 0; nty_i = 0; }
     const int64_t gy0_i = gy0 + top;
+    int64_t nty_i = ylim - gy0_i >= g.cfg.TH ? cdiv(ylim - gy0_i, g.cfg.TH) : 0;
+    if (txB <= txA || nty_i <= 0) { txA = txB = 0; nty_i = 0; }
     const int64_t n_int = (int64_t)nframes * g.npl * nty_i * (txB - txA);
+    // x-edge kernel (Group::xedge): the tile columns outside [txA, txB) of the interior tile rows
+    const bool xe = K.fn_e && nty_i > 0;
+    const int64_t n_edge = xe ? (int64_t)nframes * g.npl * nty_i * (g.ntx - (txB - txA)) : 0;
+    const int64_t bxA = xe ? 0 : txA, bxB = xe ? g.ntx : txB;   // the border kernel's excluded columns
     const int64_t nty_b = (gy1 - gy0 + THb - 1) / THb;
-    const int64_t tyA_b = nty_i > 0 ? top / THb : 0, tyB_b = nty_i > 0 ? tyA_b + nty_i * g.cfg.TH / THb : 0;
-    // x-border kernel: the side tile columns of the interior rows in TH_x-row tiles; the border kernel then
-    // keeps only the top / bottom remainders (its excluded rectangle spans every column)
-    const bool xk = K.fn_x && g.TH_x > 0 && nty_i > 0 && (txA > 0 || txB < g.ntx);
-    const int64_t nty_x = xk ? nty_i * g.cfg.TH / g.TH_x : 0;
-    const int64_t n_x = xk ? (int64_t)nframes * g.npl * nty_x * (g.ntx - (txB - txA)) : 0;
-    const int64_t bxA = xk ? 0 : txA, bxB = xk ? g.ntx : txB;
+    const int64_t tyA_b = nty_i > 0 ? top / THb : 0, tyB_b = nty_i > 0 ? (ylim - gy0) / THb : 0;
     const int64_t n_bdr = (int64_t)nframes * g.npl * (nty_b * g.ntx - (tyB_b - tyA_b) * (bxB - bxA));
+    const int32_t ylast = nty_i > 0 ? (int32_t)(ylim - g.cfg.TH) : INT32_MAX;
     (void)nty;
     void* args[] = {buf.data()};
+    // diagnosis only (PMG_DIAG_SKIP = "b" / "e" / "i" letters): skip the border / x-edge / interior launches to
+    // time the others alone (the output is then incomplete)
+    static const char* skip = getenv("PMG_DIAG_SKIP");
     auto launch = [&](CUfunction f, int bps, int64_t nt, CUstream st, const char* what) {
-      const bool bd = f == K.fn_b, xx = f == K.fn_x;
-      int32_t ints[14] = {Hg, Wg, (int32_t)(bd ? gy0 : gy0_i), gy1, (int32_t)(bd ? nty_b : xx ? nty_x : nty_i), (int32_t)g.ntx,
+      const bool bd = f == K.fn_b;
+      if (skip && std::strchr(skip, bd ? 'b' : f == K.fn_e ? 'e' : 'i')) return;
+      int32_t ints[16] = {Hg, Wg, (int32_t)(bd ? gy0 : gy0_i), gy1, (int32_t)(bd ? nty_b : nty_i), (int32_t)g.ntx,
                           (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0, (int32_t)(bd ? bxA : txA), (int32_t)(bd ? bxB : txB),
-                          (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : xx ? nty_x : nty_i)};
-      std::memcpy(buf.data() + off_int, ints, 56);
+                          (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : nty_i), bd ? INT32_MAX : ylast, 0};
+      std::memcpy(buf.data() + off_int, ints, 64);
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
       CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);
       if (r != CUDA_SUCCESS) throw Error(-6, std::string("launch of ") + g.name + what + ": " + cu_err(r));
       ++P.last_launches;
     };
-    if ((n_bdr > 0 || n_x > 0) && n_int > 0) {
-      // border tiles on the lane's side stream, forked from and joined back into the lane's stream
+    if (n_int > 0 && (n_bdr > 0 || n_edge > 0)) {
+      // border / x-edge tiles on the lane's side streams, forked from and joined back into the lane's stream.
+      // With an x-edge kernel the border kernel holds only the top / bottom tile rows: the interior kernel is
+      // launched first so that its single wave of warps is resident from the start, and the few edge and border
+      // warps fill the slots it leaves; otherwise (many x-border tiles) the border kernel goes first
       check(D.EventRecord(gfork, gs), "cuEventRecord");
       check(D.StreamWaitEvent(gside, gfork, 0), "cuStreamWaitEvent");
-      if (n_bdr > 0) launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
-      if (n_x > 0) launch(K.fn_x, K.blocks_per_sm_x, n_x, gside, "_x");
-      launch(K.fn, K.blocks_per_sm, n_int, gs, "");
+      if (n_edge > 0) check(D.StreamWaitEvent(gside2, gfork, 0), "cuStreamWaitEvent");
+      if (xe) {
+        launch(K.fn, K.blocks_per_sm, n_int, gs, "");
+        if (n_edge > 0) launch(K.fn_e, K.blocks_per_sm_e, n_edge, gside2, "_e");
+        if (n_bdr > 0) launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
+      } else {
+        launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
+        launch(K.fn, K.blocks_per_sm, n_int, gs, "");
+      }
       check(D.EventRecord(gjoin, gside), "cuEventRecord");
       check(D.StreamWaitEvent(gs, gjoin, 0), "cuStreamWaitEvent");
+      if (n_edge > 0) {
+        check(D.EventRecord(gjoin2, gside2), "cuEventRecord");
+        check(D.StreamWaitEvent(gs, gjoin2, 0), "cuStreamWaitEvent");
+      }
     } else if (n_int > 0) {
       launch(K.fn, K.blocks_per_sm, n_int, gs, "");
-    } else {
-      if (n_bdr > 0) launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gs, "_b");
-      if (n_x > 0) launch(K.fn_x, K.blocks_per_sm_x, n_x, gs, "_x");
+    } else if (n_bdr > 0) {
+      launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gs, "_b");
     }
     (void)ntiles;
   }
@@ -756,6 +805,7 @@ namespace pmg {
 // copied once (bands share their halo rows in the full-size device buffer).
 void plan_run_host(Plan& P, const pmg_buf* hin, int nin, const pmg_buf* hout, int nout, const pmg_buf* din,
                    const pmg_buf* dout, void* ws, int chunks, CUstream s) {
+  std::lock_guard<std::recursive_mutex> lock(P.run_mu);
   Drv& D = drv();
   if (!D.ok) throw Error(-6, D.err);
   const Pipeline& p = *P.pipe;

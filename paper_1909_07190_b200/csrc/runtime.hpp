@@ -1,5 +1,6 @@
 // runtime.hpp — JIT compilation (NVRTC, sm_100a), plans, workspace and stream-ordered launches.
 #pragma once
+#include <mutex>
 #include <cuda.h>
 
 #include <map>
@@ -23,7 +24,8 @@ struct Compiled {
 };
 
 // compile one group kernel for sm_100a (disk cache keyed by source + options); throws Error(PMG_ERR_NVRTC)
-Compiled jit_compile(const std::string& name, const std::string& source);
+// compile with NVRTC for sm_100a, through the on-disk cubin cache (dir_override: cache directory for this call)
+Compiled jit_compile(const std::string& name, const std::string& source, const std::string& dir_override = "");
 
 struct WsTensor {          // workspace placement of an intermediate (materialised, non-liveout) stage
   int stage = -1;
@@ -34,8 +36,8 @@ struct WsTensor {          // workspace placement of an intermediate (materialis
 struct Kernel {
   Compiled bin;
   CUmodule mod = nullptr;
-  CUfunction fn = nullptr, fn_b = nullptr, fn_x = nullptr;   // interior tiles / border tiles / x-border tiles
-  int blocks_per_sm = 0, blocks_per_sm_b = 0, blocks_per_sm_x = 0;
+  CUfunction fn = nullptr, fn_b = nullptr, fn_e = nullptr;   // interior tiles / border tiles / x-edge tiles
+  int blocks_per_sm = 0, blocks_per_sm_b = 0, blocks_per_sm_e = 0;
 };
 
 struct Plan {
@@ -59,8 +61,8 @@ struct Plan {
   int nlanes = 1;
   std::vector<int> lane_of;                // per group
   std::vector<std::vector<int>> deps;      // per group: the groups producing what it reads
-  std::vector<CUstream> lane_stream, lane_side;
-  std::vector<CUevent> lane_fork, lane_join, ev_group;
+  std::vector<CUstream> lane_stream, lane_side, lane_side2;   // side2: x-edge kernels, concurrent with the border kernel
+  std::vector<CUevent> lane_fork, lane_join, lane_join2, ev_group;
   CUevent ev_run = nullptr;
   std::string tune_json;                   // measured selection report (pmg_sched_opts.tune), empty otherwise
   int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
@@ -68,6 +70,12 @@ struct Plan {
   CUstream h2d = nullptr, d2h = nullptr;
   std::vector<CUevent> ev_in, ev_done;
   CUevent ev_start = nullptr, ev_end = nullptr;
+  bool released = false;
+  std::recursive_mutex run_mu;        // serialises the host-side enqueue of runs (shared fork/join events and side streams)
+  Plan() = default;
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+  ~Plan();   // releases every CUDA resource (modules, streams, events, the primary-context retain)
 };
 
 std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,

@@ -149,8 +149,9 @@ static double min_txs(int64_t start, int64_t nbytes, int tx) {
 // busiest warp.  The kernel cannot beat its HBM time.  Constants were fitted on B200 schedule sweeps
 // (profiles/sweep_r01_*.txt, tools/fit_weights.py).
 struct TimeModel {
-  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1800, launch_us = 1, c_border = 3, cpi_warp = 4;
+  double c0 = 10, c_stage = 2, c_stream = 0, lat_cycles = 1100, launch_us = 1, c_border = 3, cpi_warp = 6;
   double c_gather = 6;    // per gathered read per point (camera sweeps 3 / 6 / 12: profiles/camera_groupings_r01g.txt)
+  double issue_eff = 1.1; // SM issue slots per useful instruction (Harris 6400^2 interior alone: 89 % issue-active)
 };
 static TimeModel time_model() {
   TimeModel m;
@@ -247,13 +248,16 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   const double I_step = k.V * k.TX * ops + k.TX * (M.c_stage * g.gs.size() + M.c_stream * g.streams.size()) + M.c0;
   const double R = std::max(1.0, std::floor(resident_warps));
   const double lat = M.lat_cycles * 4.0 / std::max(1, k.PREF);
-  // border tiles (first/last tile rows, first/last tile columns) run concurrently in the border kernel, cut
-  // into TH_b-row tiles, through the general body (c_border x the instructions) at about half the residency
-  const double ntx = std::ceil(W / g.OW), nty = std::ceil(H / k.TH);
-  const double bt = C * (std::min(nty, 2.0) * ntx + std::max(0.0, nty - 2) * std::min(ntx, 2.0));
-  const double it = std::max(0.0, tiles - bt);
+  // border tiles run concurrently in the border kernel, in TH_b-row tiles, through the general body (c_border x
+  // the instructions) at about half the residency: the top rows and the bottom tile row (the interior's last
+  // tile row is shifted up to end at the image), plus -- without x-edge tiles -- the first / last tile columns
   const int THb = g.TH_b > 0 ? g.TH_b : k.TH;
-  const double btb = bt * k.TH / THb, Rb = std::max(1.0, std::floor(R / 2));
+  const double ntx = std::ceil(W / g.OW);
+  const double nty_i = H - 2.0 * THb >= k.TH ? std::ceil((H - 2.0 * THb) / k.TH) : 0.0;
+  const double ntx_i = g.xedge ? ntx : std::max(0.0, ntx - 2);
+  const double it = C * nty_i * ntx_i;
+  const double btb = nty_i > 0 ? C * (2 * ntx + (g.xedge ? 0.0 : 2 * nty_i * k.TH / THb)) : C * std::ceil(H / THb) * ntx;
+  const double Rb = std::max(1.0, std::floor(R / 2));
   // SM issue bound: the busiest SM issues ceil(tiles / NSMs) tiles' instructions at 4 per clock;
   // warp latency bound: the busiest warp walks ceil(tiles / (R * NSMs)) tiles at <= 1 instruction per clock
   // and no faster than the ring delivers rows
@@ -262,7 +266,7 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   const double t_warp = std::max(std::ceil(it / (R * S.nsms)) * g.nsteps * std::max(I_step * M.cpi_warp, lat),
                                  std::ceil(btb / (Rb * S.nsms)) * (THb - g.t_first) *
                                      std::max(I_step * M.c_border * M.cpi_warp, lat));
-  const double t_issue = std::max(t_sm, t_warp) / S.sm_clock_hz;
+  const double t_issue = std::max(t_sm * M.issue_eff, t_warp) / S.sm_clock_hz;
   double bytes = 0;
   for (auto& st : g.streams) bytes += (double)(k.TH + st.hi - st.lo) * st.row_elems * st.esz;
   for (auto& P : g.gs)
@@ -316,7 +320,20 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
   //  extraTBs  = idle fraction of the last wave of tiles, 1 - waves / ceil(waves) (0 below one wave, where the
   //              shortfall is already in the occupancy term).
   const double slots = c.occupancy * S.max_warps_per_sm, tiles_ = c.total_threads / S.warp_size;
-  c.est_us = slots > 0 ? est_time_us(A, g, S, slots, &c, bands) : std::numeric_limits<double>::infinity();
+  // the time model counts the warps the hardware really keeps resident: registers are allocated per warp in
+  // units of 256 from the register file of one of the 4 SM sub-partitions (16K registers each), blocks need
+  // their shared memory plus 1 KB of reserve, at most 32 blocks and 64 warps per SM
+  double hw_slots = 0;
+  {
+    const int r = std::max(8, ((int)std::ceil(c.reg_per_th) + 7) / 8 * 8);
+    const int per_smsp = (int)(S.regs_per_sm / 4) / (r * 32);
+    const int nw = std::max(1, k.NW);
+    const int64_t by_regs = (int64_t)(4 * per_smsp) / nw;
+    const int64_t by_smem = S.shmem_per_sm / std::max<int64_t>(1, g.block_smem + 1024);
+    const int64_t blocks = std::min<int64_t>({by_regs, by_smem, (int64_t)S.max_tb_per_sm, (int64_t)(S.max_warps_per_sm / nw)});
+    hw_slots = (double)(blocks * nw);
+  }
+  c.est_us = slots > 0 && hw_slots > 0 ? est_time_us(A, g, S, hw_slots, &c, bands) : std::numeric_limits<double>::infinity();
   if (slots > 0) {
     c.occupancy = std::min(slots, tiles_ / S.nsms) / S.max_warps_per_sm;
     const double waves = tiles_ / (slots * S.nsms);
@@ -348,7 +365,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                  const pmg_sched_opts& o, CostBreakdown* out, const RegProbe* probe) {
   std::vector<int> Vs = o.vec > 0 ? std::vector<int>{o.vec} : std::vector<int>{1, 2, 4};
   std::vector<int> TXs = o.chunks > 0 ? std::vector<int>{o.chunks} : std::vector<int>{1, 2, 4};
-  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 48, 64, 96};
+  std::vector<int> THs = o.rows > 0 ? std::vector<int>{o.rows} : std::vector<int>{8, 16, 24, 32, 48, 64, 80, 96, 100, 112, 128};
   // NW: OTPW warps are independent, so the block size only sets the register budget ptxas plans for; one warp
   // per block was fastest or tied in every B200 sweep (profiles/sweep_r05_*), larger blocks via the override
   std::vector<int> NWs = o.warps > 0 ? std::vector<int>{o.warps} : std::vector<int>{1};
