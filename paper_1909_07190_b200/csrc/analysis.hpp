@@ -49,6 +49,12 @@ std::string describe_pipeline(const Analysis& A);
 std::shared_ptr<Pipeline> inline_expanding(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
                                            std::vector<std::string>* inlined);
 
+// phase.cpp: alignment & scaling of downsampling edges -- a stage read only as S(2v + b) along y or x by
+// readers of half its extent is replaced by its two phases at the readers' extent (exact; names of the split
+// stages, "name/y" or "name/x", appended to *split).  PMG_PHASE_SPLIT=0 disables it.
+std::shared_ptr<Pipeline> phase_split(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
+                                      std::vector<std::string>* split);
+
 // ---- paper §4 formulas (warp geometry, scratchpads, overlap) ----
 std::array<int, 3> warp_sizes(const std::array<int, 3>& B, int warp_size);
 

@@ -138,11 +138,14 @@ pmg_status pmg_pipeline_describe(pmg_pipeline p, const int64_t* params, int npar
 pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap, size_t* needed) {
   if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
   PMG_TRY({
-    std::vector<std::string> names;
+    std::vector<std::string> names, split;
     auto q = inline_expanding(p->p, pvec(params, nparams), &names);
+    q = phase_split(q, pvec(params, nparams), &split);
     std::ostringstream o;
     o << "{\"inlined\":[";
     for (size_t i = 0; i < names.size(); ++i) o << (i ? "," : "") << "\"" << names[i] << "\"";
+    o << "],\"split\":[";
+    for (size_t i = 0; i < split.size(); ++i) o << (i ? "," : "") << "\"" << split[i] << "\"";
     o << "],\"text\":\"";
     for (char c : q->source) {
       if (c == '\n') o << "\\n";
@@ -209,7 +212,7 @@ void pmg_sched_opts_default(pmg_sched_opts* o) {
 static std::shared_ptr<Pipeline> effective(const std::shared_ptr<Pipeline>& p, const std::vector<int64_t>& params,
                                            const pmg_sched_opts* opts) {
   if (opts && opts->no_inline) return p;
-  return inline_expanding(p, params, nullptr);
+  return phase_split(inline_expanding(p, params, nullptr), params, nullptr);
 }
 
 static void spec_or_default(const pmg_gpu_spec* s, const pmg_weights* w, pmg_gpu_spec& S, pmg_weights& W) {

@@ -167,6 +167,29 @@ std::string inline_one(const Analysis& A, int P) {
 
 }  // namespace
 
+// text printing shared with phase.cpp (the rewrites produce pipeline text that is parsed again)
+std::string print_expr_text(const Pipeline& p, const std::vector<std::string>& vars, const Expr& e, const Hook* hook) {
+  return print(p, vars, e, hook);
+}
+
+std::string print_pipeline_text(const Pipeline& p, const std::vector<std::string>& stage_lines,
+                                const std::vector<std::string>& liveouts) {
+  std::ostringstream o;
+  if (!p.params.empty()) {
+    o << "param ";
+    for (size_t i = 0; i < p.params.size(); ++i) o << (i ? ", " : "") << p.params[i];
+    o << "\n";
+  }
+  for (auto& im : p.images) o << "image " << im.name << "(" << print_ext(p, im.extents) << "): " << dtype_name(im.dtype) << "\n";
+  for (auto& t : p.tables)
+    o << "table " << t.name << "(" << print(p, {}, *t.extent, nullptr) << "): " << dtype_name(t.dtype) << "\n";
+  for (auto& l : stage_lines) o << l << "\n";
+  o << "liveout ";
+  for (size_t i = 0; i < liveouts.size(); ++i) o << (i ? ", " : "") << liveouts[i];
+  o << "\n";
+  return o.str();
+}
+
 std::shared_ptr<Pipeline> inline_expanding(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
                                            std::vector<std::string>* inlined) {
   for (int guard = 0; guard < 256; ++guard) {

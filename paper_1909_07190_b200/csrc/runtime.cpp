@@ -312,7 +312,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     return best;
   }
   auto P = std::make_unique<Plan>();
-  if (!(opts && opts->no_inline)) p = inline_expanding(p, params, &P->inlined);
+  if (!(opts && opts->no_inline)) p = phase_split(inline_expanding(p, params, &P->inlined), params, &P->split);
   P->pipe = p;
   P->A = analyze(*p, params);
   P->device = device;
@@ -368,6 +368,8 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   std::ostringstream js;
   js << "{\"inlined\":[";
   for (size_t i = 0; i < P->inlined.size(); ++i) js << (i ? "," : "") << "\"" << P->inlined[i] << "\"";
+  js << "],\"split\":[";
+  for (size_t i = 0; i < P->split.size(); ++i) js << (i ? "," : "") << "\"" << P->split[i] << "\"";
   js << "],\"schedule\":" << P->sch.json << ",\"kernels\":[";
   for (size_t gi = 0; gi < P->sch.groups.size(); ++gi) {
     Group& g = P->sch.groups[gi];

@@ -277,7 +277,8 @@ def test_nvrtc_sm100a_sass_census(tmp_path):
 
 @pytest.mark.parametrize("wl", [PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": 96, "H": 64}, 1005),
                                 PI.small("local_laplacian", 256, 128), PI.small("camera", 96, 64),
-                                PI.small("harris", 64, 48)], ids=lambda w: w.pipeline)
+                                PI.small("harris", 64, 48), PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 64, "H": 48}, 1006)],
+                         ids=lambda w: w.pipeline)
 def test_inlining_preserves_the_definition(wl):
     """The inlining pass (inline.cpp) rewrites the pipeline text; the oracle evaluates the rewritten text and
     the text as written, and the liveouts must agree bit for bit (clamped substitution, stored-value casts)."""
@@ -292,5 +293,34 @@ def test_inlining_preserves_the_definition(wl):
         np.testing.assert_array_equal(a[k].view(np.uint8), b[k].view(np.uint8))
     if "laplacian" in wl.pipeline:
         assert "gP0" in r["inlined"] and "lP0" in r["inlined"]      # the 8-plane full-resolution stages
+        assert "gDx1/y" in r["split"]                               # phase split of the downsample pairs
+    elif "pyramid" in wl.pipeline:
+        assert "ADx1/y" in r["split"]
     else:
         assert r["inlined"] == []                                   # nothing data-expanding to substitute
+    if "camera" in wl.pipeline:
+        assert r["split"] == ["denoised/y", "denoised_ye/x", "denoised_yo/x"]
+
+
+PHASE = """param W, H
+image img(H, W): f32
+stage s(y, x) [H, W]: f32 = img(y, x) * 2.0 + img(y, x + 1)
+stage c(y, x) [H / 2, W / 2]: f32 = ((((((s(2*y-3, 2*x) + 0.5 * s(2*y-2, 2*x+1)) + 0.25 * s(2*y-1, 2*x-1)) + s(2*y, 2*x) * 3.0) + s(2*y+1, 2*x+2)) + s(2*y+2, 2*x-2) * 0.125) + s(2*y+3, 2*x+3))
+liveout c
+"""
+
+
+@pytest.mark.parametrize("W,H", [(2, 2), (4, 6), (10, 8), (6, 16), (12, 14)])
+def test_phase_split_exact_at_every_edge(W, H):
+    """Alignment & scaling by phase splitting (phase.cpp): a stage read only as s(2v + b) is replaced
+    by its two phases; reads with b in [-3, 3] exercise both edge selects (q >= 1 at the high edge, q <= -1 at the
+    low edge) in both dims at sizes down to 2 x 2.  The oracle must give the same bits for both texts."""
+    import numpy as np
+    from oracle import evaluate
+    p = pmg.Pipeline(PHASE)
+    r = p.inlined({"W": W, "H": H})
+    assert r["split"] == ["s/y", "s_ye/x", "s_yo/x"]
+    img = np.random.default_rng(W * 100 + H).random((H, W), dtype=np.float32)
+    a = evaluate(PHASE, {"W": W, "H": H}, {"img": img})["c"]
+    b = evaluate(r["text"], {"W": W, "H": H}, {"img": img})["c"]
+    np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
