@@ -249,14 +249,16 @@ def test_band_input_rows_suffice(wl, n):
 def test_emitted_kernels_use_only_warp_synchronisation(name):
     """OTPW "does not employ thread block synchronization at all"."""
     wl = PI.WORKLOADS[name]
-    e = pmg.Pipeline(wl.text).emit(wl.params, opts=pmg.sched_opts(probe=False))
+    pipe = pmg.Pipeline(wl.text)
+    one = [0] * len(pipe.stages) if name == "harris" else None      # the fully fused Harris group
+    e = pipe.emit(wl.params, opts=pmg.sched_opts(probe=False, group_of_stage=one))
     for g in e["groups"]:
         src = g["source"]
         assert "__syncthreads" not in src and "bar.sync" not in src
         if "pmg_mbar_wait" in src:       # groups staging inputs through the warp's TMA ring
             assert "__syncwarp" in src
     if name == "harris":
-        assert "pmg_shfl(" in e["groups"][0]["source"]      # load types (3)/(4): neighbour-lane registers
+        assert any("pmg_shfl(" in g["source"] for g in e["groups"])   # load types (3)/(4): neighbour-lane registers
 
 
 @pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not available")
@@ -264,8 +266,9 @@ def test_nvrtc_sm100a_sass_census(tmp_path):
     """Compile the Harris group for sm_100a on the host (NVRTC, no GPU) and inspect the SASS: TMA bulk
     copies (UBLKCP) + mbarriers (SYNCS), warp shuffles (SHFL), no block barrier (BAR.*), no spills."""
     wl = PI.WORKLOADS["harris"]
-    opts = pmg.sched_opts(vec=4, chunks=1, rows=24, warps=4, prefetch=8, probe=False)
-    rep = pmg.Pipeline(wl.text).precompile(wl.params, str(tmp_path), opts=opts)
+    pipe = pmg.Pipeline(wl.text)
+    opts = pmg.sched_opts(vec=4, chunks=1, rows=24, warps=4, prefetch=8, probe=False, group_of_stage=[0] * len(pipe.stages))
+    rep = pipe.precompile(wl.params, str(tmp_path), opts=opts)
     k = rep["kernels"][0]
     assert k["spill_stores"] == 0 and k["regs"] > 0
     cubins = list(tmp_path.glob("*.cubin"))
