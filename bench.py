@@ -288,6 +288,7 @@ def main():
     ap.add_argument("--no-tune", action="store_true",
                     help="use the cost model's schedule instead of measured selection (pmg_sched_opts.tune)")
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config lines (C1, C3, C4, C5, PB)")
+    ap.add_argument("--frames", type=int, default=4096, help="C1 blur: frames in the batch (split across ranks)")
     args = ap.parse_args()
     wl = PI.WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -310,8 +311,14 @@ def main():
     torch.cuda.init()
     stream = torch.cuda.current_stream(dev)
 
-    nb = args.simulate_bands if (world == 1 and args.simulate_bands > 1) else world
-    band = nb // 2 if nb != world else rank
+    # C1 blur runs as a batch of frames, split per GPU by contiguous frame ranges; the other
+    # workloads are single images split into row bands
+    frames_total = args.frames if wl.name == "blur" else 0
+    from paper_1909_07190_b200.dist import frame_range, gather_bands, gather_frames
+    f0, f1 = frame_range(rank, world, frames_total) if frames_total else (0, 0)
+    nf = f1 - f0
+    nb = 1 if frames_total else (args.simulate_bands if (world == 1 and args.simulate_bands > 1) else world)
+    band = 0 if frames_total else (nb // 2 if nb != world else rank)
     # schedule for this rank's band size; measured selection (tune) among the model's schedule and its neighbours
     opts = pmg.sched_opts(bands=max(nb, 0), tune=not args.no_tune)
     if args.opts:
@@ -325,23 +332,35 @@ def main():
 
     from gpu_util_bench import device_inputs
     o_r0, o_r1, i_r0, i_r1 = plan.band_rows(band, nb)
+    all_bands = [plan.band_rows(b, nb)[:2] for b in range(nb)]
     # rotating buffer sets: together at least 2x L2, so no run finds its inputs in L2 (bands are small at N>1)
     set_bytes = sum(int(np.prod(io.shape[:-2])) * (i_r1 - i_r0) * io.shape[-1] * pmg._binding.DTYPE_SIZE[io.dtype]
                     for io in plan.inputs if not io.is_table) + \
         sum(int(np.prod(o.shape[:-2])) * (o_r1 - o_r0) * o.shape[-1] * pmg._binding.DTYPE_SIZE[o.dtype] for o in plan.outputs)
+    set_bytes *= max(1, nf)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     sets = max(2, -(-2 * l2 // max(1, set_bytes)))
     in_sets, out_sets = [], []
+    if frames_total:
+        src = torch.from_numpy(PI.blur_frames(frames_total)[f0:f1])
     for _ in range(sets):
+        if frames_total:
+            x = pmg.empty_pitched((nf, *plan.inputs[0].shape), "f32", f"cuda:{dev}")
+            x.copy_(src.to(f"cuda:{dev}"))
+            in_sets.append([x])
+            out_sets.append(plan.alloc_outputs(nf))
+            continue
         ins = device_inputs(plan, inputs_np, dev, rows=(i_r0, i_r1) if nb > 1 else None)
         outs = [pmg.empty_pitched((*o.shape[:-2], o_r1 - o_r0, o.shape[-1]), o.dtype, f"cuda:{dev}") for o in plan.outputs]
         in_sets.append(ins)
         out_sets.append(outs)
-    ws = plan.workspace()
+    ws = plan.workspace(max(1, nf))
 
     def launch(i, st):
         ins, outs = in_sets[i % sets], out_sets[i % sets]
-        if nb > 1:
+        if frames_total:
+            plan.run_batch(ins, outs, ws, st)
+        elif nb > 1:
             plan.run_band(band, nb, ins, outs, ws, st)
         else:
             plan.run(ins, outs, ws, st)
@@ -415,23 +434,72 @@ def main():
     nk = plan.num_kernels
     bytes_in = sum(int(np.prod(io.shape)) * pmg._binding.DTYPE_SIZE[io.dtype] for io in plan.inputs)
     bytes_out = sum(int(np.prod(io.shape)) * pmg._binding.DTYPE_SIZE[io.dtype] for io in plan.outputs)
-    algo_bytes = (bytes_in + bytes_out) / nb
+    share = nf if frames_total else 1.0 / nb        # this rank's part of the work, in images
+    algo_bytes = (bytes_in + bytes_out) * share
     pk, pk_kind = peaks()
     peak_hbm = float(pk["hbm_gbs"])
     # algorithmic ALU work: every operation of the definition as written, over each stage's domain
     dsc = pipe.describe(wl.params)
-    algo_ops = sum(st["ops"] * int(np.prod(st["extent"])) for st in dsc["stages"]) / nb
+    algo_ops = sum(st["ops"] * int(np.prod(st["extent"])) for st in dsc["stages"]) * share
     nsms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_alu = 128 * nsms * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12      # FP32/INT32 lane-ops, T/s
     t_hbm = algo_bytes / (peak_hbm * 1e9)
     t_alu = algo_ops / (peak_alu * 1e12)
     hbm_achieved = algo_bytes / (ms * 1e-3) / 1e9
     alu_achieved = algo_ops / (ms * 1e-3) / 1e12
-    value = W * H / (ms * 1e-3) / 1e6
+    value = W * H * max(1, frames_total) / (ms * 1e-3) / 1e6
+
+    # on-request assembly (north_star: NCCL only gathers bands or frames where the caller asks): one
+    # all_gather_into_tensor of this rank's output rows / frames, timed separately (not part of `value`)
+    gather = None
+    if world > 1:
+        out0 = out_sets[0][0]
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gms = []
+        for _ in range(3):
+            g0.record(stream)
+            full = gather_frames(out0, frames_total) if frames_total else gather_bands(out0, all_bands)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            gms.append(g0.elapsed_time(g1))
+        t = torch.tensor([min(gms)], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather = {"ms": float(t.item()), "collective": "torch.distributed.all_gather_into_tensor (NCCL)",
+                  "bytes_assembled": int(full.numel() * full.element_size()),
+                  "note": "assembled output on every rank; timed after the compute loop, excluded from value"}
+        del full
 
     # end-to-end through the public API with host buffers: pinned H2D of the inputs + run + D2H of the output
     e2e = None
-    if nb == 1:
+    if frames_total and world == 1:
+        fbytes_in = nf * int(np.prod(plan.inputs[0].shape)) * 4
+        fbytes_out = nf * int(np.prod(plan.outputs[0].shape)) * 4
+        host_in = torch.from_numpy(PI.blur_frames(frames_total)).pin_memory()
+        host_out = torch.empty((nf, *plan.outputs[0].shape), dtype=torch.float32).pin_memory()
+        ins, outs = in_sets[0], out_sets[0]
+
+        def e2e_step():
+            # the public API on host frames: pinned H2D copy of the batch, pmg_run_batch, D2H copy of the outputs
+            ins[0].copy_(host_in, non_blocking=True)
+            plan.run_batch(ins, outs, ws, stream)
+            host_out.copy_(outs[0], non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n_e2e = max(3, args.steps // 4)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / n_e2e
+        e2e = {"value": W * H * frames_total / (ems * 1e-3) / 1e6, "unit": "Mpixels/s", "h2d_bytes_per_step": fbytes_in,
+               "d2h_bytes_per_step": fbytes_out, "ms_per_step": ems,
+               "api": "pmg_run_batch (C ABI) with pinned host frames copied in / out on the stream"}
+    elif nb == 1:
         host_in = [torch.from_numpy(np.ascontiguousarray(inputs_np[io.name]).view(
             {np.dtype(np.uint16): np.int16}.get(inputs_np[io.name].dtype, inputs_np[io.name].dtype))).pin_memory()
             for io in plan.inputs]
@@ -472,7 +540,7 @@ def main():
         "metric": metric_name(wl), "value": value, "unit": "Mpixels/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded U[0,1) image, pmg_inputs.py)",
+        "data": "synthetic (seeded images, pmg_inputs.py)",
         "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
                    "launch": ("CUDA graph replay per buffer set" if use_graph else "host launches") +
                              (" (faster in warm-up: graph %.4f / host %.4f ms)" % (launch_mode[True], launch_mode[False])
@@ -496,6 +564,11 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    if gather:
+        line["gather"] = gather
+    if frames_total:
+        line["config"]["frames"] = f"batch of {frames_total} frames, {nf} on rank 0 (contiguous frame ranges per rank)"
+        line["config"]["parallelism"] = f"frames x{world}"
     if nb != world:
         line["config"]["simulated_bands"] = f"band {band} of {nb} timed on one GPU; value = whole image / band time"
     if not args.no_cpu_baseline and world == 1 and nb == 1:

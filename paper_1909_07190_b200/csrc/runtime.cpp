@@ -183,7 +183,7 @@ static int64_t round_up64(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 
 // device time of one run of plan Q on synthetic inputs (measured selection, pmg_sched_opts.tune): buffers
 // are allocated here, filled with a constant byte pattern, 2 warm-up runs, then the best of 3 samples of 10 runs
-static double time_plan_us(Plan& Q) {
+static double time_plan_us(Plan& Q, int nbands = 1) {
   Drv& D = drv();
   const Pipeline& p = *Q.pipe;
   const Analysis& A = Q.A;
@@ -215,18 +215,26 @@ static double time_plan_us(Plan& Q) {
   }
   for (int s : p.liveouts) out.push_back(buf_of(A.stage_ext[s], p.stages[s].dtype));
   void* ws = Q.ws_bytes ? (void*)(uintptr_t)alloc(Q.ws_bytes) : nullptr;
+  // plans made for row bands (sched_opts.bands = n) are timed on the middle band, as one rank runs it: the
+  // buffers point at the band's first input / output row of the full-size allocations
+  const int band = nbands > 1 ? nbands / 2 : -1;
+  if (band >= 0) {
+    BandRows br = band_rows(Q, band, nbands);
+    for (size_t i = 0; i < p.images.size(); ++i) in[i].ptr = (char*)in[i].ptr + br.in_r0 * in[i].row_pitch_bytes;
+    for (auto& o : out) o.ptr = (char*)o.ptr + br.out_r0 * o.row_pitch_bytes;
+  }
   CUstream st;
   check(D.StreamCreate(&st, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
   CUevent e0, e1;
   check(D.EventCreate(&e0, 0), "cuEventCreate");
   check(D.EventCreate(&e1, 0), "cuEventCreate");
-  for (int r = 0; r < 2; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, -1, 0, 1, nullptr, nullptr);
+  for (int r = 0; r < 2; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, band, nbands, 1, nullptr, nullptr);
   // the paper's statistic: the minimum over samples of the mean of back-to-back runs
   const int R = 10;
   float ms = 1e30f;
   for (int sample = 0; sample < 3; ++sample) {
     check(D.EventRecord(e0, st), "cuEventRecord");
-    for (int r = 0; r < R; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, -1, 0, 1, nullptr, nullptr);
+    for (int r = 0; r < R; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, band, nbands, 1, nullptr, nullptr);
     check(D.EventRecord(e1, st), "cuEventRecord");
     check(D.EventSynchronize(e1), "cuEventSynchronize");
     float m = 0;
@@ -251,7 +259,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     // greedy: each round times every neighbour merge of the current best schedule and moves to the fastest,
     // until no merge helps (at most 4 rounds)
     CtxGuard g(best->ctx);
-    double tb = time_plan_us(*best);
+    double tb = time_plan_us(*best, opts->bands);
     std::ostringstream js;
     js << "{\"candidates\":[{\"round\":0,\"groups\":" << best->sch.groups.size() << ",\"us\":" << tb << "}";
     int chosen = 0, pos = 0;
@@ -270,7 +278,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
         } catch (const Error&) {
           continue;   // a merge the geometry cannot build (e.g. a non-constant dependence)
         }
-        double t = time_plan_us(*Q);
+        double t = time_plan_us(*Q, opts->bands);
         js << ",{\"round\":" << round << ",\"groups\":" << Q->sch.groups.size() << ",\"us\":" << t << "}";
         ++pos;
         if (t < rt) { rt = t; rbest = std::move(Q); chosen = pos; }
@@ -300,7 +308,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
           } catch (const Error&) {
             continue;
           }
-          double t = time_plan_us(*Q);
+          double t = time_plan_us(*Q, opts->bands);
           js << ",{\"round\":\"config\",\"V\":" << q[0] << ",\"TX\":" << q[1] << ",\"TH\":" << th << ",\"us\":" << t << "}";
           ++pos;
           if (t < ct) { ct = t; cbest = std::move(Q); chosen = pos; }
