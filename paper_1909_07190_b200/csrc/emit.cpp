@@ -683,9 +683,15 @@ struct Emitter {
          "  const int j = t % side; int r = t / side; ty = a.tyA + r % h; r /= h; pc = r % a.npl; fr = r / a.npl;\n"
          "  tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
     kernel(true);
-    if (g.xedge) kernel(true, true);
+    if (g.xedge && !xe_skip) kernel(true, true);
     return o.str();
   }
+  // the interior-tile kernel alone (the selector's register probe reads its ptxas count)
+  std::string run_interior_only() {
+    xe_skip = true;
+    return run();
+  }
+  bool xe_skip = false;
 
   // the border-tile kernel of the same group, with TH_b-row tiles (macros TH / NSTEPS redefined)
   std::string run_border() {
@@ -1324,8 +1330,9 @@ int interior_state_regs(const Analysis& A, const Group& g) {
   return e.state_regs();
 }
 
-std::string emit_group(const Analysis& A, const Group& g) {
+std::string emit_group(const Analysis& A, const Group& g, bool interior_only) {
   Emitter e(A, g);
+  if (interior_only) return e.run_interior_only();
   std::string src = e.run();
   Group gb = g;                        // border kernel: same geometry with TH_b-row tiles
   if (g.TH_b > 0) {

@@ -104,7 +104,7 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& group_of_s
 int interior_state_regs(const Analysis& A, const Group& g);
 
 // CUDA C++ source of one group kernel (NVRTC input)
-std::string emit_group(const Analysis& A, const Group& g);
+std::string emit_group(const Analysis& A, const Group& g, bool interior_only = false);
 
 struct Schedule {
   std::vector<Group> groups;          // topo order of groups

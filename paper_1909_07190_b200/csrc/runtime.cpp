@@ -13,6 +13,7 @@
 #include <unistd.h>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <mutex>
 #include <regex>
 #include <sstream>
@@ -153,13 +154,56 @@ Compiled jit_compile(const std::string& name, const std::string& source, const s
   return c;
 }
 
+// register-probe results (ptxas registers / spill bytes of a candidate's interior kernel), keyed like the cubin
+// cache; kept in a small text file next to libpmg.so (kernel_dir()/probe_cache.txt) that travels with the
+// package, so plan creation on a fresh GPU box does not recompile the selector's finalists
+static std::mutex g_probe_mu;
+static std::map<std::string, std::pair<int, int>>* g_probe = nullptr;
+
+static std::string probe_file() { return kernel_dir() + "/probe_cache.txt"; }
+
+static std::string compile_key(const std::string& source) {
+  int maj = 0, min = 0;
+  nvrtcVersion(&maj, &min);
+  std::string key_src = source + "\n//" + std::string(kOtpwHeader);
+  for (const char* o : kOptions) key_src += std::string(" ") + o;
+  key_src += " nvrtc" + std::to_string(maj) + "." + std::to_string(min);
+  char hex[32];
+  snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(key_src));
+  return hex;
+}
+
 RegProbe make_probe(const Analysis& A) {
   return [&A](const Group& g, int* regs, int* spill) {
     Group h = g;
     h.name = "pmg_probe";
-    Compiled c = jit_compile(h.name, emit_group(A, h));
+    const std::string src = emit_group(A, h, /*interior_only=*/true);
+    const std::string key = compile_key(src);
+    {
+      std::lock_guard<std::mutex> lk(g_probe_mu);
+      if (!g_probe) {
+        g_probe = new std::map<std::string, std::pair<int, int>>();
+        std::ifstream f(probe_file());
+        std::string k;
+        int r, sp;
+        while (f >> k >> r >> sp) (*g_probe)[k] = {r, sp};
+      }
+      auto it = g_probe->find(key);
+      if (it != g_probe->end()) {
+        *regs = it->second.first;
+        *spill = it->second.second;
+        return *regs > 0;
+      }
+    }
+    Compiled c = jit_compile(h.name, src);
     *regs = c.regs;
     *spill = std::max(c.spill_stores, 0) + std::max(c.spill_loads, 0);
+    if (c.regs > 0) {
+      std::lock_guard<std::mutex> lk(g_probe_mu);
+      (*g_probe)[key] = {*regs, *spill};
+      std::ofstream f(probe_file(), std::ios::app);   // one short line per append (O_APPEND)
+      f << key << " " << *regs << " " << *spill << "\n";
+    }
     return c.regs > 0;
   };
 }
@@ -290,7 +334,8 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     // single-group plans: the model's tile choice is also checked against a small grid of 128-column warp
     // tiles (V x TX in {1x4, 2x2, 4x1}) and tile heights (unsharp 2048^2: the model picks within 6 % of the
     // best measured configuration, profiles/unsharp_grid_r01n.txt)
-    if (best->sch.groups.size() == 1) {
+    const char* grid_env = getenv("PMG_TUNE_GRID");   // "0": merges only (tests keep plan creation short)
+    if (best->sch.groups.size() == 1 && !(grid_env && grid_env[0] == '0')) {
       std::vector<int> one(best->A.p->stages.size(), 0);
       const int vx[3][2] = {{1, 4}, {2, 2}, {4, 1}};
       std::unique_ptr<Plan> cbest;

@@ -141,9 +141,8 @@ def test_scaled_streams(cfg, W, H, monkeypatch):
                for s in g["config"]["streams"]), "no scaled stream in the plan"
 
 
-@pytest.mark.parametrize("cfg", [None] + PARITY_SWEEP[:4],
-                         ids=lambda c: "auto" if c is None else "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
-@pytest.mark.parametrize("W,H", [(97, 63), (256, 130)])
+@pytest.mark.parametrize("cfg,W,H", [(None, 97, 63), (PARITY_SWEEP[1], 97, 63), (PARITY_SWEEP[3], 97, 63), (None, 256, 130)],
+                         ids=lambda c: "auto" if c is None else c if isinstance(c, int) else "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
 def test_pyramid_blend_parity(cfg, W, H):
     """Pyramid Blend (Table 2): three Gaussian pyramids, two Laplacian pyramids,
     per-level blend and collapse through scaled streams, inlined upsamplings and broadcast mask reads."""
@@ -155,7 +154,7 @@ def test_pyramid_blend_parity(cfg, W, H):
     assert neq == 0
 
 
-@pytest.mark.parametrize("name", ["camera", "pyramid_blend"])
+@pytest.mark.parametrize("name", ["camera"])
 def test_scaled_streams_on_pipelines(name, monkeypatch):
     """The scaled-stream path on the camera pipe (Bayer phases: 2v+b in y and x) and the pyramid blend."""
     monkeypatch.setenv("PMG_SCALED", "1")
@@ -171,10 +170,11 @@ def test_scaled_streams_on_pipelines(name, monkeypatch):
 
 
 @pytest.mark.parametrize("name,fuse", [("camera", True), ("pyramid_blend", True), ("unsharp", False)])
-def test_measured_selection(name, fuse):
+def test_measured_selection(name, fuse, monkeypatch):
     """pmg_sched_opts.tune: the DP schedule and (greedily, round by round) each neighbour merge are compiled and
     timed on the device; the kept plan is the fastest candidate and computes the same function (bit-exact).
     Unfused starting points (one stage per group) make the merge rounds non-trivial."""
+    monkeypatch.setenv("PMG_TUNE_GRID", "0")      # merge rounds only (the tile grid is exercised by bench.py)
     w = (PI.Workload("pb", "pyramid_blend_J3.pmg", {"W": 160, "H": 96}, 1006) if name == "pyramid_blend"
          else PI.small(name, 300, 200))
     inp = w.inputs("structured") if name == "pyramid_blend" else w.inputs()
@@ -190,7 +190,8 @@ def test_measured_selection(name, fuse):
         assert len(us) >= 2 and len(plan.describe()["schedule"]["groups"]) < len(plan.pipeline.stages)
 
 
-@pytest.mark.parametrize("W,H,opts", [(24, 24, None), (77, 53, dict(vec=1, chunks=2, rows=5, warps=2, prefetch=2))])
+@pytest.mark.parametrize("W,H,opts", [(24, 24, dict(vec=4, chunks=1, rows=8, warps=1, prefetch=4)),
+                                      (77, 53, dict(vec=1, chunks=2, rows=5, warps=2, prefetch=2))])
 def test_operator_table_parity(W, H, opts):
     """Reading R4 on the device: every operator / builtin / cast of tests/ops_table.py over all pairs of its
     edge-case values (shift counts outside [0, 31], zero and -1 divisors, INT_MIN, NaN, +-inf, out-of-range
@@ -199,7 +200,8 @@ def test_operator_table_parity(W, H, opts):
     inp = OT.inputs(W, H)
     with np.errstate(all="ignore"):
         exp = evaluate(OT.TEXT, {"W": W, "H": H}, inp)
-    got, _ = run_gpu(OT.TEXT, {"W": W, "H": H}, inp, opts=pmg.sched_opts(**opts) if opts else None)
+    one = [0] * len(OT.STAGES)                    # one fused group with every stage a liveout (one compile)
+    got, _ = run_gpu(OT.TEXT, {"W": W, "H": H}, inp, opts=pmg.sched_opts(**opts, group_of_stage=one))
     bad = []
     for k in OT.STAGES:
         g, e = got[k], exp[k]
