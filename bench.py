@@ -575,7 +575,7 @@ def main():
         line["cpu_baseline"] = cpu_baseline(wl)
     if not args.no_per_config and world == 1 and nb == 1 and not args.opts:
         per = {}
-        for name in ["blur", "unsharp", "camera", "local_laplacian", "pyramid_blend"]:
+        for name in ["blur", "unsharp", "camera", "local_laplacian", "pyramid_blend", "multiscale_interp"]:
             if name == args.workload:
                 continue
             try:

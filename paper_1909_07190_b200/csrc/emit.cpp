@@ -555,6 +555,9 @@ struct Emitter {
     return {std::string(f) + "(" + tof(left).s + ", " + b.s + ")", Kind::Float};
   }
 
+  // OTPTB ablation (PMG_OTPTB=1): block barriers between stages instead of warp-only synchronisation
+  static bool otptb() { const char* e = getenv("PMG_OTPTB"); return e && e[0] == '1'; }
+
   bool pack_on() const {
     // opt-in (PMG_PACK=1): bit-exact, but on B200 the make_float2 MOVs cost what the packed FADD2s save
     // (harris 6400^2: 0.1198 ms packed vs 0.1169 ms scalar)
@@ -754,9 +757,17 @@ struct Emitter {
          "  (void)ring; (void)bar0; (void)ring_addr;\n"
          "  const int gw = blockIdx.x * NW + wib;\n"
          "  const int nwt = gridDim.x * NW;\n"
-         "  if (gw >= a.ntiles) return;\n"
-         "  const int H = a.H, W = a.W;\n"
-         "  const int my_tiles = (a.ntiles - gw + nwt - 1) / nwt;\n";
+         "  const int H = a.H, W = a.W;\n";
+    if (otptb()) {
+      // OTPTB ablation (§3, Fig. 8): the block's warps step through their tiles together and meet at
+      // a block barrier after every stage; all warps of a block take the same number of tiles (a warp past the
+      // last tile recomputes the last tile and stores the same values)
+      o << "  if (blockIdx.x * NW >= a.ntiles) return;\n"
+           "  const int my_tiles = (a.ntiles - blockIdx.x * NW + nwt - 1) / nwt;\n";
+    } else {
+      o << "  if (gw >= a.ntiles) return;\n"
+           "  const int my_tiles = (a.ntiles - gw + nwt - 1) / nwt;\n";
+    }
     const bool hs = !g.streams.empty();
     if (hs) {
       // ---- TMA producer state: one request per step, PREF steps ahead of the consumer; lane 0 issues ----
@@ -790,7 +801,7 @@ struct Emitter {
           << "      tot += byt" << j << ";\n    }\n";
       }
       o << "  };\n";
-      o << "  p_params(gw, p_y0, p_total";
+      o << "  p_params(" << (otptb() ? "min(gw, a.ntiles - 1)" : "gw") << ", p_y0, p_total";
       for (size_t j = 0; j < g.streams.size(); ++j) o << ", p_src" << j << ", p_dst" << j << ", p_bytes" << j;
       o << ");\n";
       // prologue: the first PREF requests of the first tile
@@ -804,7 +815,7 @@ struct Emitter {
       o << "  }\n  int c_slot = 0;\n  u32 phase = 0u;   // parity of the ring's current lap (all slots are used round-robin)\n";
     }
     o << "  for (int it = 0; it < my_tiles; ++it) {\n"
-         "    const int tile = gw + it * nwt;\n"
+         "    const int tile = " << (otptb() ? "min(gw + it * nwt, a.ntiles - 1)" : "gw + it * nwt") << ";\n"
          "    int tx, ty, pc, fr;\n    " << dec << "(a, tile, tx, ty, pc, fr);\n"
          "    const int y0 = " << y0_expr("ty") << ";\n"
          "    const int cx = " << cx_expr("tx") << ";\n"
@@ -827,7 +838,7 @@ struct Emitter {
          "    (void)pc; (void)fr; (void)xL; (void)xLh; (void)xb; (void)yend;\n";
     if (hs) {
       o << "    const bool has_next = it + 1 < my_tiles;\n"
-           "    if (has_next) p_params(tile + nwt, pn_y0, pn_total";
+           "    if (has_next) p_params(" << (otptb() ? "min(gw + (it + 1) * nwt, a.ntiles - 1)" : "tile + nwt") << ", pn_y0, pn_total";
       for (size_t j = 0; j < g.streams.size(); ++j) o << ", pn_src" << j << ", pn_dst" << j << ", pn_bytes" << j;
       o << ");\n";
     }
@@ -1035,7 +1046,7 @@ struct Emitter {
       }
       o << ind << "}\n";
     }
-    o << ind << "}\n" << ind << "__syncwarp();\n";
+    o << ind << "}\n" << ind << (otptb() ? "__syncthreads();\n" : "__syncwarp();\n");
   }
 
   // refill the slot read in this step with the request PREF steps ahead (next tile when it crosses NSTEPS)
@@ -1315,6 +1326,7 @@ struct Emitter {
           o << in2 << "}\n";
         }
       o << ind << "}\n";
+      if (otptb()) o << ind << "__syncthreads();   // OTPTB ablation: block barrier between stages\n";
     }
     if (!g.streams.empty()) refill(tconst, tval, rmode, ind);
     o << ind << "}\n";

@@ -47,6 +47,15 @@ def structured(shape, seed):
     return out
 
 
+def sparse_rgba(h, w, seed, variant="uniform", density=0.1):
+    """Multiscale Interpolation input: colour planes (uniform or structured) and an alpha plane that is 1 on a
+    seeded ~10 % of the pixels (the known samples) and 0 elsewhere (at least one sample)."""
+    rgb = structured((3, h, w), seed) if variant != "uniform" else uniform((3, h, w), seed)
+    alpha = (np.random.default_rng(seed + 7).random((h, w)) < density).astype(np.float32)
+    alpha[h // 2, w // 2] = 1.0
+    return np.ascontiguousarray(np.concatenate([rgb, alpha[None]], axis=0))
+
+
 def blend_mask(h, w):
     """Pyramid-blend mask: 0 on the left, 1 on the right, a linear ramp over the middle eighth of the width."""
     x = (np.arange(w, dtype=np.float64) - (w - 1) / 2.0) / max(1.0, w / 8.0) + 0.5
@@ -138,6 +147,8 @@ class Workload:
             K = 8 if self.pipeline == "local_laplacian.pmg" else int(self.pipeline.split("K")[-1].split(".")[0])
             img = structured((3, H, W), s) if variant != "uniform" else uniform((3, H, W), s)
             return {"inp": img, "remap": ll_remap(K)}
+        if self.pipeline.startswith("multiscale_interp"):
+            return {"inp": sparse_rgba(H, W, s, variant)}
         if self.pipeline.startswith("pyramid_blend"):
             return {"A": structured((3, H, W), s), "B": structured((3, H, W), s + 1) if variant != "uniform"
                     else uniform((3, H, W), s + 1), "M": blend_mask(H, W)}
@@ -160,6 +171,9 @@ WORKLOADS = {
     "camera": Workload("camera", "camera.pmg", {"W": 2528, "H": 1920}, 1004, "C4 2528x1920 u16 Bayer"),
     "local_laplacian": Workload("local_laplacian", "local_laplacian.pmg", {"W": 2560, "H": 1536}, 1005,
                                 "C5 2560x1536x3 f32, J=8, K=8"),
+    # PAPER.md Table 2 l.1148 (not a BASELINE.json config)
+    "multiscale_interp": Workload("multiscale_interp", "multiscale_interp.pmg", {"W": 2560, "H": 1536}, 1007,
+                                  "MI 2560x1536 RGBA -> 3 planes f32, J=10"),
     # PAPER.md Table 2 l.1150 (not a BASELINE.json config)
     "pyramid_blend": Workload("pyramid_blend", "pyramid_blend.pmg", {"W": 3840, "H": 2160}, 1006,
                               "PB 3840x2160x3 f32, J=4"),

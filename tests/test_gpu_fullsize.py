@@ -1,8 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, WHOLE IMAGES, element by element, in the launch configurations
 bench.py times:
 
-* C2 Harris 6400², C3 unsharp 2048²×3, C4 camera 2528×1920, C5 local Laplacian 2560×1536×3 and Pyramid Blend
-  3840×2160×3 — automatic schedule, whole image, one run on the caller's stream (bench.py N=1);
+* C2 Harris 6400², C3 unsharp 2048²×3, C4 camera 2528×1920, C5 local Laplacian 2560×1536×3, Pyramid Blend
+  3840×2160×3 and Multiscale Interpolation 2560×1536 (RGBA) — automatic schedule, whole image, one run on the caller's stream (bench.py N=1);
 * row bands (bench.py N>1, schedule for one band) — every band of N = 8 (Harris, local Laplacian) and N = 4
   (camera) run separately, stitched, compared with the whole-image oracle;
 * C1 blur 128² as the 4096-frame batch (pmg_run_batch) of bench.py's per-config line.
@@ -22,8 +22,9 @@ pytestmark = pytest.mark.gpu
 import paper_1909_07190_b200 as pmg  # noqa: E402
 
 TOL = {"blur": dict(float_tol=1e-4), "unsharp": dict(float_tol=1e-4), "harris": dict(rel_range=1e-5),
-       "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4)}
-VARIANT = {"local_laplacian": "structured", "pyramid_blend": "structured"}
+       "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4),
+       "multiscale_interp": dict(float_tol=1e-4)}
+VARIANT = {"local_laplacian": "structured", "pyramid_blend": "structured", "multiscale_interp": "structured"}
 
 _ORACLE = {}
 
@@ -42,7 +43,7 @@ def assert_identical(name, got, exp, what=""):
     assert neq == 0, f"{name}{what}: {neq} of {exp.size} outputs differ from the oracle (max {d})"
 
 
-@pytest.mark.parametrize("name", ["harris", "unsharp", "camera", "local_laplacian", "pyramid_blend"])
+@pytest.mark.parametrize("name", ["harris", "unsharp", "camera", "local_laplacian", "pyramid_blend", "multiscale_interp"])
 def test_fullsize_whole_image_parity(name):
     import torch
     wl = PI.WORKLOADS[name]

@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 import paper_1909_07190_b200 as pmg  # noqa: E402
 
 TOL = {"blur": dict(float_tol=1e-4), "unsharp": dict(float_tol=1e-4), "harris": dict(rel_range=1e-5),
-       "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4)}
+       "local_laplacian": dict(float_tol=1e-4), "camera": {}, "pyramid_blend": dict(float_tol=1e-4),
+       "multiscale_interp": dict(float_tol=1e-4)}
 
 
 def check(name, W, H, opts=None, variant="uniform", bit_exact=True):
@@ -235,3 +236,16 @@ def test_xedge_kernel_parity(name, W, H, cfg):
     image.  Widths divisible by V so the edge kernel is used (checked), bit-exact against the oracle."""
     plan = check(name, W, H, opts=pmg.sched_opts(**cfg, tx_size=32) if cfg else None)
     assert all(k["edge_regs"] > 0 for k in plan.describe()["kernels"]), plan.describe()["kernels"]
+
+
+@pytest.mark.parametrize("cfg,W,H", [(None, 96, 64), (PARITY_SWEEP[2], 96, 64), (None, 160, 96)],
+                         ids=lambda c: "auto" if c is None else c if isinstance(c, int) else "V{vec}TX{chunks}TH{rows}P{prefetch}".format(**c))
+def test_multiscale_interp_parity(cfg, W, H):
+    """Multiscale Interpolation (Table 2 l.1148; reading R23): premultiplied pull-push
+    pyramid over sparse RGBA samples, J = 4 levels, bit-exact against the oracle."""
+    w = PI.Workload("mi", "multiscale_interp_J4.pmg", {"W": W, "H": H}, 1007)
+    inp = w.inputs("structured")
+    exp = evaluate(w.text, w.params, inp)
+    got, _ = run_gpu(w.text, w.params, inp, opts=None if cfg is None else pmg.sched_opts(**cfg, tx_size=32))
+    neq, _ = compare(got["out"], exp["out"], float_tol=1e-4)
+    assert neq == 0

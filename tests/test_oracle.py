@@ -250,6 +250,50 @@ def test_pyramid_blend_shapes_and_stage_count():
     assert ev.shape_of("out") == (3, 2160, 3840)
 
 
+# ----------------------------------------------------------------------------- multiscale interpolation (NEXT-4)
+def _mi(W=96, H=64):
+    return (PI.PIPELINES / "multiscale_interp_J4.pmg").read_text(), {"W": W, "H": H}
+
+
+def test_multiscale_interp_full_alpha_is_identity():
+    """alpha == 1 everywhere: I_0 = d_0 + (1 - 1) * up = d_0 = (c * 1, 1), so out = (c * 1) / 1 = c bit for bit
+    (IEEE: x * 1 = x, 0 * finite = 0, x + 0 = x, x / 1 = x) whatever the pyramid holds."""
+    text, p = _mi()
+    rgb = PI.uniform((3, 64, 96), 11)
+    inp = np.concatenate([rgb, np.ones((1, 64, 96), np.float32)])
+    out = evaluate(text, p, {"inp": inp})["out"]
+    np.testing.assert_array_equal(out.view(np.uint32), rgb.view(np.uint32))
+
+
+def test_multiscale_interp_single_colour_fills_every_hole():
+    """Every known sample has colour v: each premultiplied plane is v * alpha, every stage is linear in its
+    inputs, so in exact arithmetic I_l(c) = v * I_l(3) at every level and out == v at every pixel (also in the
+    holes); the f64 evaluation reaches it to rounding, the f32 one to 1e-5."""
+    text, p = _mi()
+    inp = PI.sparse_rgba(64, 96, 12)
+    v = np.array([0.25, 0.5, 0.875], np.float32)
+    inp[:3] = v[:, None, None]
+    for prec, tol in [("f64", 1e-12), ("f32", 1e-5)]:
+        out = evaluate(text, p, {"inp": inp}, precision=prec)["out"]
+        assert np.max(np.abs(out - v[:, None, None])) < tol, prec
+
+
+def test_multiscale_interp_keeps_known_samples_exactly_where_alpha_is_one():
+    """Where alpha == 1, I_0 = d_0 + 0 * up_0 = (c, 1) exactly, so out(c) = c bit for bit at every sample."""
+    text, p = _mi()
+    inp = PI.sparse_rgba(64, 96, 13)
+    out = evaluate(text, p, {"inp": inp})["out"]
+    m = inp[3] == 1.0
+    np.testing.assert_array_equal(out[:, m].view(np.uint32), inp[:3][:, m].view(np.uint32))
+
+
+def test_multiscale_interp_shapes_and_stage_count():
+    prog = parse((PI.PIPELINES / "multiscale_interp.pmg").read_text())
+    assert len(prog.stages) == 47
+    ev = Evaluator(prog, {"W": 2560, "H": 1536})
+    assert ev.shape_of("pd9") == (4, 3, 5) and ev.shape_of("out") == (3, 1536, 2560)
+
+
 # ----------------------------------------------------------------------------- f32 vs exact arithmetic
 @pytest.mark.parametrize("name,W,H,tol", [("blur", 40, 30, 1e-6), ("unsharp", 40, 30, 1e-5),
                                           ("harris", 40, 30, None), ("pyramid_blend", 64, 48, 1e-5)])
