@@ -289,6 +289,7 @@ def main():
                     help="use the cost model's schedule instead of measured selection (pmg_sched_opts.tune)")
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config lines (C1, C3, C4, C5, PB)")
     ap.add_argument("--frames", type=int, default=4096, help="C1 blur: frames in the batch (split across ranks)")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) leg (ncu launch lists)")
     args = ap.parse_args()
     wl = PI.WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -473,7 +474,9 @@ def main():
 
     # end-to-end through the public API with host buffers: pinned H2D of the inputs + run + D2H of the output
     e2e = None
-    if frames_total and world == 1:
+    if args.no_e2e:
+        pass
+    elif frames_total and world == 1:
         fbytes_in = nf * int(np.prod(plan.inputs[0].shape)) * 4
         fbytes_out = nf * int(np.prod(plan.outputs[0].shape)) * 4
         host_in = torch.from_numpy(PI.blur_frames(frames_total)).pin_memory()
