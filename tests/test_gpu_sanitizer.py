@@ -22,7 +22,7 @@ def test_compute_sanitizer(tool):
         pytest.skip("compute-sanitizer not available")
     env = dict(os.environ, PYTORCH_NO_CUDA_MEMORY_CACHING="1")
     cases = ["harris", "camera", "ll"] if tool in ("memcheck", "initcheck") else ["harris", "camera"]
-    extra = ["--track-unused-memory", "no"] if tool == "initcheck" else []
+    extra = []
     cmd = [SAN, "--tool", tool, "--error-exitcode", "99", *extra, sys.executable, str(ROOT / "tools" / "sanitize_run.py"), *cases]
     r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
     tail = (r.stdout + r.stderr)[-3000:]
