@@ -341,7 +341,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
       std::unique_ptr<Plan> cbest;
       double ct = tb;
       for (auto& q : vx)
-        for (int th : {24, 32, 48, 64, 96, 100, 112, 128}) {
+        for (int th : {16, 24, 32, 48, 64, 96, 100, 112, 128}) {
           pmg_sched_opts oc = o0;
           oc.group_of_stage = one.data();
           oc.vec = q[0];

@@ -13,4 +13,9 @@ for wl in unsharp camera local_laplacian multiscale_interp; do
   timeout 600 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv --log-file gpurun_out/$tag/launches_$wl.csv \
     python tools/run_once.py $wl auto 3 > /dev/null 2>&1
 done
-for f in gpurun_out/$tag/*_full.ncu-rep; do echo $f; done
+# keep the raw-page CSV of every capture (small); the .ncu-rep files themselves stay on the box except Harris's
+for f in gpurun_out/$tag/*_full.ncu-rep; do
+  ncu -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null
+  case $f in *harris_full*) ;; *) rm -f $f ;; esac
+done
+ls -la gpurun_out/$tag/

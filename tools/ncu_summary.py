@@ -67,8 +67,11 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    if str(path).endswith(".csv"):   # a raw-page CSV exported on the GPU box (ncu -i X.ncu-rep --page raw --csv)
+        out = Path(path).read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units, data = rows[0], rows[1], rows[2:]
     ks = []
