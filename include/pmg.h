@@ -130,6 +130,9 @@ typedef struct {
                            then takes seconds per candidate; runs are unaffected.  A B200 refinement outside the
                            paper's model-based selector. */
   int32_t reserved;
+  const double* time_per_iter;  /* NULL = static operation counts; else per stage (declaration order) the measured
+                                   TimePerIter in seconds (pmg_profile_stages) used by Alg. 2's
+                                   compute term (cost_model 1); stages the schedule rewrote keep the static count */
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);
@@ -219,6 +222,14 @@ pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, 
  * buffers must stay valid until then.  Input images must have the liveouts' row extent. */
 pmg_status pmg_run_host(pmg_plan plan, const pmg_buf* host_in, int nin, const pmg_buf* host_out, int nout,
                         const pmg_buf* dev_in, const pmg_buf* dev_out, void* workspace, int chunks, void* stream);
+
+/* on-device TimePerIter microbenchmarks (§6 l.890-898: "TimePerIter ... obtained by running each stage
+ * in isolation"): every stage of the pipeline as written runs as its own kernel (one stage per group, no
+ * inlining) on synthetic inputs of the given extents; each kernel is timed alone (CUDA events, best of 3 samples
+ * of 10 runs).  JSON {"stages":[{"name","points","us","time_per_iter","regs"}]}; time_per_iter = us / points, the
+ * per-point time of the stage's standalone kernel (memory included).  Needs the device. */
+pmg_status pmg_profile_stages(pmg_pipeline p, const int64_t* params, int nparams, int device, char* json, size_t cap,
+                              size_t* needed);
 
 /* device self-test of the warp-shuffle semantics of Fig. 1: lane 0 receives the sum */
 pmg_status pmg_selftest_shuffle(int device, int32_t* lane0_sum);

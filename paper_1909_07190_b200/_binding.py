@@ -68,7 +68,7 @@ class SchedOpts(C.Structure):
                 ("smem_chunks", C.c_int32), ("rows", C.c_int32), ("warps", C.c_int32), ("prefetch", C.c_int32),
                 ("tx_size", C.c_int32), ("budget", C.c_int32), ("fuse", C.c_int32), ("regcap", C.c_int32),
                 ("probe", C.c_int32), ("cost_model", C.c_int32), ("bands", C.c_int32), ("no_inline", C.c_int32),
-                ("tune", C.c_int32), ("reserved", C.c_int32)]
+                ("tune", C.c_int32), ("reserved", C.c_int32), ("time_per_iter", C.POINTER(C.c_double))]
 
 
 P = C.c_void_p
@@ -89,6 +89,7 @@ _sig = {
     "pmg_gpu_spec_query": (C.c_int, [C.c_int, C.c_double, C.POINTER(GpuSpec)]),
     "pmg_weights_preset": (C.c_int, [C.c_char_p, C.POINTER(Weights)]),
     "pmg_sched_opts_default": (None, [C.POINTER(SchedOpts)]),
+    "pmg_profile_stages": (C.c_int, [P, I64P, C.c_int, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "pmg_schedule": (C.c_int, [P, I64P, C.c_int, C.POINTER(GpuSpec), C.POINTER(Weights), C.POINTER(SchedOpts),
                                C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "pmg_analyze_group": (C.c_int, [P, I64P, C.c_int, C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -234,6 +234,8 @@ pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, cons
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
+    std::vector<double> tpi = map_time_per_iter(*p->p, *eff, o.time_per_iter);
+    if (o.time_per_iter) o.time_per_iter = tpi.data();
     RegProbe probe = make_probe(A);
     Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     return put_json(sch.json, json, cap, needed);
@@ -284,6 +286,8 @@ pmg_status pmg_emit(pmg_pipeline p, const int64_t* params, int nparams, const pm
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
+    std::vector<double> tpi = map_time_per_iter(*p->p, *eff, o.time_per_iter);
+    if (o.time_per_iter) o.time_per_iter = tpi.data();
     RegProbe probe = make_probe(A);
     Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     std::string out = "{\"schedule\":" + sch.json + ",\"groups\":[";
@@ -315,6 +319,8 @@ pmg_status pmg_precompile(pmg_pipeline p, const int64_t* params, int nparams, co
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
+    std::vector<double> tpi = map_time_per_iter(*p->p, *eff, o.time_per_iter);
+    if (o.time_per_iter) o.time_per_iter = tpi.data();
     RegProbe probe = make_probe(A);
     Schedule sch = schedule(A, S, W, o, o.probe ? &probe : nullptr);
     std::string out = "{\"schedule\":" + sch.json + ",\"kernels\":[";
@@ -343,6 +349,33 @@ void pmg_plan_destroy(pmg_plan plan) {
   if (!plan) return;
   try { plan_destroy(plan->plan.get()); } catch (...) {}
   delete plan;
+}
+
+pmg_status pmg_profile_stages(pmg_pipeline p, const int64_t* params, int nparams, int device, char* json, size_t cap,
+                              size_t* needed) {
+  if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
+  PMG_TRY({
+    pmg_sched_opts o;
+    pmg_sched_opts_default(&o);
+    o.fuse = 0;        // one stage per group: every stage is its own kernel
+    o.no_inline = 1;   // the pipeline as written
+    auto P = plan_create(p->p, pvec(params, nparams), device, nullptr, nullptr, &o);
+    std::vector<double> us = profile_groups_us(*P);
+    std::ostringstream js;
+    js << "{\"stages\":[";
+    for (size_t gi = 0; gi < P->sch.groups.size(); ++gi) {
+      const Group& g = P->sch.groups[gi];
+      const int s = g.stages.at(0);
+      int64_t pts = 1;
+      for (int d = 0; d < 3; ++d)
+        if (P->A.stage_ext[s].has[d]) pts *= P->A.stage_ext[s].e[d];
+      js << (gi ? "," : "") << "{\"name\":\"" << p->p->stages[s].name << "\",\"index\":" << s << ",\"points\":" << pts
+         << ",\"us\":" << us[gi] << ",\"time_per_iter\":" << us[gi] * 1e-6 / (double)pts << ",\"regs\":"
+         << P->kernels[gi].bin.regs << "}";
+    }
+    js << "]}";
+    return put_json(js.str(), json, cap, needed);
+  })
 }
 
 pmg_status pmg_plan_describe(pmg_plan plan, char* buf, size_t cap, size_t* needed) {
@@ -406,6 +439,8 @@ pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams
     pmg_sched_opts o;
     if (opts) o = *opts;
     else pmg_sched_opts_default(&o);
+    std::vector<double> tpi = map_time_per_iter(*p->p, *P.pipe, o.time_per_iter);
+    if (o.time_per_iter) o.time_per_iter = tpi.data();
     P.sch = schedule(P.A, S, W, o, nullptr);
     BandRows b = band_rows(P, band, nbands);
     if (out_r0) *out_r0 = b.out_r0;

@@ -291,6 +291,17 @@ static double time_plan_us(Plan& Q, int nbands = 1) {
   return 1000.0 * ms / R;
 }
 
+std::vector<double> profile_groups_us(Plan& P) {
+  CtxGuard g(P.ctx);
+  std::vector<double> us(P.sch.groups.size(), 0.0);
+  struct Reset { Plan& P; ~Reset() { P.only_group = -1; } } reset{P};
+  for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) {
+    P.only_group = (int)gi;
+    us[gi] = time_plan_us(P);
+  }
+  return us;
+}
+
 std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,
                                   const pmg_gpu_spec* spec, const pmg_weights* w, const pmg_sched_opts* opts) {
   Drv& D = drv();
@@ -365,6 +376,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     return best;
   }
   auto P = std::make_unique<Plan>();
+  std::shared_ptr<Pipeline> written = p;
   if (!(opts && opts->no_inline)) p = phase_split(inline_expanding(p, params, &P->inlined), params, &P->split);
   P->pipe = p;
   P->A = analyze(*p, params);
@@ -393,6 +405,8 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     o.fuse = 1;
     o.probe = 1;
   }
+  std::vector<double> tpi = map_time_per_iter(*written, *P->pipe, o.time_per_iter);
+  if (o.time_per_iter) o.time_per_iter = tpi.data();
   RegProbe probe = make_probe(P->A);
   P->sch = schedule(P->A, P->spec, P->weights, o, o.probe ? &probe : nullptr);
   const Pipeline& pp = *p;
@@ -673,6 +687,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     for (int l = 1; l < P.nlanes; ++l) check(D.StreamWaitEvent(P.lane_stream[l], P.ev_run, 0), "cuStreamWaitEvent");
   }
   for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) {
+    if (P.only_group >= 0 && (int)gi != P.only_group) continue;
     const Group& g = P.sch.groups[gi];
     Kernel& K = P.kernels[gi];
     const int lane = lanes ? P.lane_of[gi] : 0;

@@ -67,6 +67,7 @@ struct Plan {
   CUevent ev_run = nullptr;
   std::string tune_json;                   // measured selection report (pmg_sched_opts.tune), empty otherwise
   int last_launches = 0;                   // kernels launched by the most recent plan_run (bench evidence)
+  int only_group = -1;                     // >= 0: plan_run launches that group alone (profile_groups_us)
   // host-buffer runs (pmg_run_host): copy streams and per-chunk events, created on first use
   CUstream h2d = nullptr, d2h = nullptr;
   std::vector<CUevent> ev_in, ev_done;
@@ -89,6 +90,10 @@ BandRows band_rows(const Plan& P, int band, int nbands);
 // launch every group kernel; band < 0: full image; nframes >= 1 (batch)
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace, CUstream s,
               int band, int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs);
+
+// per-group kernel time of one run (each group launched alone on synthetic inputs; CUDA events, best of 3 samples
+// of 10 runs): the TimePerIter microbenchmark of pmg_profile_stages when groups are single stages
+std::vector<double> profile_groups_us(Plan& P);
 
 // host buffers in and out, pipelined in `chunks` row bands over copy-in / compute / copy-out streams
 void plan_run_host(Plan& P, const pmg_buf* hin, int nin, const pmg_buf* hout, int nout, const pmg_buf* din,

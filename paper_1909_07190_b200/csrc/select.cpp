@@ -280,8 +280,17 @@ static double est_time_us(const Analysis& A, const Group& g, const pmg_gpu_spec&
   return std::max(t_issue, t_mem) * 1e6 + M.launch_us;
 }
 
+std::vector<double> map_time_per_iter(const Pipeline& written, const Pipeline& eff, const double* tpi) {
+  std::vector<double> r(eff.stages.size(), 0.0);
+  if (!tpi) return r;
+  for (size_t i = 0; i < eff.stages.size(); ++i)
+    for (size_t j = 0; j < written.stages.size(); ++j)
+      if (written.stages[j].name == eff.stages[i].name) r[i] = tpi[j];
+  return r;
+}
+
 CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S, const pmg_weights& w, int cost_model,
-                        int bands) {
+                        int bands, const double* tpi_measured) {
   const Pipeline& p = *A.p;
   const KConfig& k = g.cfg;
   CostBreakdown c;
@@ -308,7 +317,9 @@ CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& S
   double tpi = 0, computed = 0, useful = 0;
   for (auto& P : g.gs) {
     double pts = (double)g.CW * (k.TH + P.hi - P.lo);
-    double t = stage_ops(p, P.id) / S.sm_clock_hz;
+    // TimePerIter: the on-device microbenchmark when given (pmg_profile_stages), else the static
+    // operation count at the SM clock
+    double t = tpi_measured && tpi_measured[P.id] > 0 ? tpi_measured[P.id] : stage_ops(p, P.id) / S.sm_clock_hz;
     tpi += t * pts / (double)(g.CW * k.TH);
     computed += pts;
     useful += out_pts;
@@ -392,7 +403,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                 cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0};
                 ++count;
                 if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
-                CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model, o.bands);
+                CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model, o.bands, o.time_per_iter);
                 if (c.infinite) { why = c.why; continue; }
                 cands.push_back({cand, c});
               }
@@ -427,7 +438,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
       if (it == meas.end() || it->second.first <= 0) continue;
       Cand c = c0;
       c.g.regs_est = it->second.first;
-      c.c = b200_cost(A, c.g, S, w, o.cost_model, o.bands);
+      c.c = b200_cost(A, c.g, S, w, o.cost_model, o.bands, o.time_per_iter);
       if (it->second.second > 0) { c.c.infinite = true; c.c.why = "register spills"; c.c.cost = std::numeric_limits<double>::infinity(); }
       fin.push_back(c);
     }

@@ -35,7 +35,11 @@ double stage_ops(const Pipeline& p, int stage);
 
 // B200-mode Alg. 2 for a built group (KConfig -> paper symbols, DESIGN.md §"Selector")
 CostBreakdown b200_cost(const Analysis& A, const Group& g, const pmg_gpu_spec& spec, const pmg_weights& w,
-                        int cost_model = 0, int bands = 1);
+                        int cost_model = 0, int bands = 1, const double* time_per_iter = nullptr);
+
+// measured TimePerIter of the pipeline as written (per stage, declaration order) -> per stage of the rewritten
+// pipeline the schedule works on (matched by name; rewritten stages get 0 = the static count)
+std::vector<double> map_time_per_iter(const Pipeline& written, const Pipeline& eff, const double* tpi);
 
 // RegUsage(H) "measured with nvcc": compile a candidate and return ptxas' registers / spill bytes
 using RegProbe = std::function<bool(const Group& g, int* regs, int* spill_bytes)>;

@@ -42,7 +42,8 @@ def weights(name: str = "b200") -> B.Weights:
 
 
 def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, warps=-1, prefetch=-1, tx_size=-1,
-               budget=0, fuse=True, regcap=0, probe=True, cost_model=0, bands=0, inline=True, tune=False) -> B.SchedOpts:
+               budget=0, fuse=True, regcap=0, probe=True, cost_model=0, bands=0, inline=True, tune=False,
+               time_per_iter=None) -> B.SchedOpts:
     o = B.SchedOpts()
     B.lib.pmg_sched_opts_default(C.byref(o))
     o.vec, o.chunks, o.smem_chunks, o.rows, o.warps, o.prefetch, o.tx_size = (
@@ -55,6 +56,10 @@ def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, 
     o.bands = bands                    # expected row-band split (the estimate counts one band's tiles)
     o.no_inline = 0 if inline else 1   # substitute data-expanding stages into their readers
     o.tune = 1 if tune else 0          # measured selection among the DP schedule and its neighbour merges
+    if time_per_iter is not None:       # measured TimePerIter per stage (Pipeline.profile_stages), Alg. 2 input
+        tarr = (C.c_double * len(time_per_iter))(*time_per_iter)
+        o._keep_tpi = tarr
+        o.time_per_iter = C.cast(tarr, C.POINTER(C.c_double))
     if group_of_stage is not None:
         arr = (C.c_int32 * len(group_of_stage))(*group_of_stage)
         o._keep = arr                      # keep the array alive with the struct
@@ -128,6 +133,16 @@ class Pipeline:
         """{"inlined": [stage names], "text": pipeline text} after substituting data-expanding stages."""
         arr, n = self.param_values(params)
         return B.call_json(B.lib.pmg_pipeline_inlined, self._h, arr, n)
+
+    def profile_stages(self, params: dict, device: int = 0) -> dict:
+        """On-device TimePerIter of every stage (each stage alone as one kernel)."""
+        import json as _json
+        arr, n = self.param_values(params)
+        cap = 1 << 20                       # one call: the profile runs kernels, so no size-query round trip
+        buf = C.create_string_buffer(cap)
+        need = C.c_size_t(0)
+        B.check(B.lib.pmg_profile_stages(self._h, arr, n, device, buf, cap, C.byref(need)))
+        return _json.loads(buf.value.decode())
 
     def schedule(self, params: dict, spec=None, weights_=None, opts=None) -> dict:
         arr, n = self.param_values(params)

@@ -103,3 +103,23 @@ def test_run_host_equals_device_run(name, W, H, chunks):
     for o, h in zip(plan.outputs, host_out):
         got = h.view(torch.int16).numpy().view(np.uint16) if h.dtype == torch.uint16 else h.numpy()
         np.testing.assert_array_equal(got.view(np.uint8), ref[o.name].view(np.uint8))
+
+
+def test_time_per_iter_microbenchmarks_feed_alg2():
+    """NEXT-3 / PAPER.md l.890-898: TimePerIter measured on the device (each stage alone as one kernel) is the
+    compute input of Alg. 2 (cost_model 1); the measured profile changes the cost, and the schedule it selects
+    computes the same function (bit-exact)."""
+    wl = PI.small("harris", 640, 480)
+    pipe = pmg.Pipeline(wl.text)
+    prof = pipe.profile_stages(wl.params)
+    names = [s["name"] for s in prof["stages"]]
+    assert sorted(names) == sorted(pipe.stages)
+    assert all(s["us"] > 0 and s["time_per_iter"] > 0 and s["points"] == 640 * 480 for s in prof["stages"])
+    tpi = [next(s["time_per_iter"] for s in prof["stages"] if s["name"] == n) for n in pipe.stages]
+    static = pipe.schedule(wl.params, opts=pmg.sched_opts(cost_model=1))
+    measured = pipe.schedule(wl.params, opts=pmg.sched_opts(cost_model=1, time_per_iter=tpi))
+    ct = lambda sch: sum(g["cost"]["computeTime"] for g in sch["groups"])
+    assert ct(static) != ct(measured)
+    inp = wl.inputs()
+    got, _ = run_gpu(wl.text, wl.params, inp, opts=pmg.sched_opts(cost_model=1, time_per_iter=tpi))
+    compare(got["harris"], evaluate(wl.text, wl.params, inp)["harris"], rel_range=1e-5)
