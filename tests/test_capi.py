@@ -301,8 +301,8 @@ def test_inlining_preserves_the_definition(wl):
         assert "ADx1/y" in r["split"]
     else:
         assert r["inlined"] == []                                   # nothing data-expanding to substitute
-    if "camera" in wl.pipeline:
-        assert r["split"] == ["denoised/y", "denoised_ye/x", "denoised_yo/x"]
+    if "camera" in wl.pipeline:   # denoise -> quad-grid phases; R, G, B and their readers -> quad phases + interleave
+        assert r["split"] == ["denoised/y", "denoised_ye/x", "denoised_yo/x", "R/up-yx"]
 
 
 PHASE = """param W, H
@@ -326,4 +326,31 @@ def test_phase_split_exact_at_every_edge(W, H):
     img = np.random.default_rng(W * 100 + H).random((H, W), dtype=np.float32)
     a = evaluate(PHASE, {"W": W, "H": H}, {"img": img})["c"]
     b = evaluate(r["text"], {"W": W, "H": H}, {"img": img})["c"]
+    np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+UPSPLIT = """param W, H
+image lo(H / 2, W / 2): f32
+image img(H, W): f32
+stage up(y, x) [H, W]: f32 = select(y % 2 == 0, lo(y / 2, x / 2), lo((y + 1) / 2, (x - 1) / 2) * 0.5)
+stage up2(y, x) [H, W]: f32 = lo((y - 1) / 2, x / 2) + select(x % 2 == 1, 1.0, 2.0)
+stage c(y, x) [H, W]: f32 = ((((up(y - 1, x) + up(y + 2, x + 1)) + up(y, x - 2)) + up(y - 2, x + 2)) * img(y, x) + up(y + 1, x - 1)) + ((((up2(y, x - 2) + up2(y + 1, x)) + up2(y - 1, x + 1)) + up2(y, x)) * 0.5 + up2(y + 2, x - 1))
+liveout c
+"""
+
+
+@pytest.mark.parametrize("W,H", [(4, 4), (6, 8), (10, 12), (16, 6)])
+def test_up_split_exact_at_every_edge(W, H):
+    """Upsampling edges (phase.cpp, reader split): stages using y, x only as (v + b) / 2 and (v + b) % 2 become four
+    quad-resolution phases, their reader c too (reads at offsets -2..2 exercise the edge selects in both dims), and
+    the liveout is rebuilt as the interleave of its phases.  The oracle must give the same bits for both texts."""
+    import numpy as np
+    from oracle import evaluate
+    p = pmg.Pipeline(UPSPLIT)
+    r = p.inlined({"W": W, "H": H})
+    assert r["inlined"] == [] and r["split"] == ["up/up-yx"]
+    rng = np.random.default_rng(W * 31 + H)
+    inp = {"lo": rng.random((H // 2, W // 2), dtype=np.float32), "img": rng.random((H, W), dtype=np.float32)}
+    a = evaluate(UPSPLIT, {"W": W, "H": H}, inp)["c"]
+    b = evaluate(r["text"], {"W": W, "H": H}, inp)["c"]
     np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
