@@ -372,6 +372,86 @@ std::string up_split(const Analysis& A, const Up& u, std::set<std::string>* inte
   return print_pipeline_text(p, lines, lo);
 }
 
+// ---- plane split (a colour-matrix mix of several plane-less producers) ------------------------------------------
+// A stage S with a small plane dimension (K <= 4 planes) that reads at least three distinct plane-less stages (the
+// camera's corrected(c) = M[c] . (R, G, B)) would be fused with them only as "broadcast" stages recomputed for every
+// plane, or read them back from HBM once per plane.  Its K planes S_k(y, x) = S(k, y, x) are plane-less stages
+// (the plane variable substituted by the constant k: exact); readers with the same K planes that read S at their
+// own plane (the tone curve) are split the same way, and every other read S(e, y, x) becomes the select chain
+// over clamp(e, 0, K-1) (reading R1), so the liveout keeps its planes.
+struct PlaneSplit { int s = -1; int K = 0; std::set<int> set; };
+
+PlaneSplit plane_candidate(const Analysis& A) {
+  const Pipeline& p = *A.p;
+  for (int s : p.topo) {
+    const Ext3& se = A.stage_ext[s];
+    if (!se.has[0] || se.e[0] > 4 || se.e[0] < 2) continue;
+    if (std::find(p.liveouts.begin(), p.liveouts.end(), s) != p.liveouts.end()) continue;
+    std::set<int> flat;
+    for (const ReadSite& r : A.reads)
+      if (r.consumer == s && r.src_is_stage && !A.stage_ext[r.src].has[0]) flat.insert(r.src);
+    if (flat.size() < 3) continue;
+    PlaneSplit ps;
+    ps.s = s;
+    ps.K = (int)se.e[0];
+    std::vector<int> work{s};
+    ps.set.insert(s);
+    while (!work.empty()) {
+      int m = work.back();
+      work.pop_back();
+      for (const ReadSite& r : A.reads) {
+        if (!r.src_is_stage || r.src != m) continue;
+        const Ext3& ce = A.stage_ext[r.consumer];
+        const bool lo = std::find(p.liveouts.begin(), p.liveouts.end(), r.consumer) != p.liveouts.end();
+        if (!lo && ce.has[0] && ce.e[0] == ps.K && r.form[0] == Form::UNIT && r.off[0] == 0 && ps.set.insert(r.consumer).second)
+          work.push_back(r.consumer);
+      }
+    }
+    return ps;
+  }
+  return {};
+}
+
+std::string plane_split_one(const Analysis& A, const PlaneSplit& ps) {
+  const Pipeline& p = *A.p;
+  using Hook = std::function<bool(const Expr&, std::string&)>;
+  std::vector<std::string> lines;
+  for (size_t sidx = 0; sidx < p.stages.size(); ++sidx) {
+    const StageDecl& sd = p.stages[sidx];
+    const int nd = (int)sd.vars.size();
+    const bool member = ps.set.count((int)sidx) > 0;
+    for (int k = 0; k < (member ? ps.K : 1); ++k) {
+      std::vector<std::string> vars = sd.vars;
+      if (member) vars[0] = std::to_string(k);          // the plane variable is the constant k
+      Hook hook = [&](const Expr& e, std::string& out) {
+        if (e.op != Expr::ACCESS || !e.is_stage || !ps.set.count(e.index)) return false;
+        const StageDecl& md = p.stages[e.index];
+        std::string rest;
+        for (size_t i = 1; i < e.args.size(); ++i) rest += ", " + print_expr_text(p, vars, *e.args[i], &hook);
+        auto nm = [&](int q) { return md.name + "_c" + std::to_string(q) + "(" + rest.substr(2) + ")"; };
+        if (member) {   // a member reads a member at its own plane: the same constant plane
+          out = nm(k);
+          return true;
+        }
+        const std::string ce = "clamp(" + print_expr_text(p, vars, *e.args[0], &hook) + ", 0, " + std::to_string(ps.K - 1) + ")";
+        std::string chain = nm(ps.K - 1);
+        for (int q = ps.K - 2; q >= 0; --q) chain = "select(" + ce + " == " + std::to_string(q) + ", " + nm(q) + ", " + chain + ")";
+        out = chain;
+        return true;
+      };
+      std::string vs, ext;
+      for (int i = member ? 1 : 0; i < nd; ++i) vs += std::string(vs.empty() ? "" : ", ") + sd.vars[i];
+      for (int i = member ? 1 : 0; i < nd; ++i)
+        ext += std::string(ext.empty() ? "" : ", ") + print_expr_text(p, {}, *sd.extents[i], nullptr);
+      lines.push_back("stage " + sd.name + (member ? "_c" + std::to_string(k) : std::string()) + "(" + vs + ") [" + ext +
+                      "]: " + dtype_name(sd.dtype) + " = " + print_expr_text(p, vars, *sd.expr, &hook));
+    }
+  }
+  std::vector<std::string> lo;
+  for (int s : p.liveouts) lo.push_back(p.stages[s].name);
+  return print_pipeline_text(p, lines, lo);
+}
+
 }  // namespace
 
 std::shared_ptr<Pipeline> phase_split(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
@@ -402,6 +482,13 @@ std::shared_ptr<Pipeline> phase_split(std::shared_ptr<Pipeline> p, const std::ve
       if (split) split->push_back(p->stages[sp.s].name + (sp.d == 1 ? "/y" : "/x"));
       p = parse_pipeline(split_one(B, sp));
     }
+  }
+  for (int guard = 0; guard < 8; ++guard) {
+    Analysis A = analyze(*p, params);
+    PlaneSplit ps = plane_candidate(A);
+    if (ps.s < 0) break;
+    if (split) split->push_back(p->stages[ps.s].name + "/planes");
+    p = parse_pipeline(plane_split_one(A, ps));
   }
   return p;
 }

@@ -302,7 +302,8 @@ def test_inlining_preserves_the_definition(wl):
     else:
         assert r["inlined"] == []                                   # nothing data-expanding to substitute
     if "camera" in wl.pipeline:   # denoise -> quad-grid phases; R, G, B and their readers -> quad phases + interleave
-        assert r["split"] == ["denoised/y", "denoised_ye/x", "denoised_yo/x", "R/up-yx"]
+        assert r["split"] == ["denoised/y", "denoised_ye/x", "denoised_yo/x", "R/up-yx", "corrected_ye_xe/planes",
+                              "corrected_yo_xe/planes", "corrected_ye_xo/planes", "corrected_yo_xo/planes"]
 
 
 PHASE = """param W, H
