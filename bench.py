@@ -161,10 +161,9 @@ def measure_config(name, dev, steps, warmup, tune=True):
     pipe = pmg.Pipeline(wl.text)
     t0 = time.perf_counter()
     probe = pmg.Plan(pipe, wl.params, device=dev)                 # model schedule: is it one group?
-    # measured selection (merge rounds, and the tile grid for one-group plans) where it stays cheap: plans of at
-    # most 6 groups (the pyramids' 20-40 groups would time hundreds of candidate plans)
-    small = len(probe.describe()["schedule"]["groups"]) <= 6
-    plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(tune=True)) if (tune and small) else probe
+    # measured selection: merge rounds (for plans of many groups only merges touching the 4 slowest groups), and
+    # the tile grid for one-group plans
+    plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(tune=True)) if tune else probe
     t_plan = time.perf_counter() - t0
     frames = 4096 if name == "blur" else 0
     nfr = max(1, frames)

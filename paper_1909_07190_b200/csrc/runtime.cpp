@@ -16,6 +16,7 @@
 #include <map>
 #include <mutex>
 #include <regex>
+#include <set>
 #include <sstream>
 
 #include "cudrv.hpp"
@@ -321,6 +322,24 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
     std::vector<std::vector<int>> keep;   // group_of_stage arrays must outlive the plans built from them
     for (int round = 1; round <= 4; ++round) {
       std::vector<std::vector<int>> cands = merge_candidates(best->A, best->sch);
+      // plans of many groups (the pyramids): only merges touching the 4 slowest groups of the current plan, timed
+      // one group at a time (profile_groups_us), keep plan creation to a few dozen candidates
+      if (best->sch.groups.size() > 6) {
+        std::vector<double> gus = profile_groups_us(*best);
+        std::vector<int> order(gus.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return gus[a] > gus[b]; });
+        std::set<int> slow(order.begin(), order.begin() + std::min<size_t>(4, order.size()));
+        std::vector<std::vector<int>> kept{cands[0]};
+        for (size_t c = 1; c < cands.size(); ++c) {
+          // candidate c merges groups g and g+1 of the current plan: find g from the array
+          int g = -1;   // the merged pair (g, g+1): the smallest new label among the relabelled stages
+          for (size_t st = 0; st < cands[c].size(); ++st)
+            if (cands[c][st] != cands[0][st] && (g < 0 || cands[c][st] < g)) g = cands[c][st];
+          if (g < 0 || slow.count(g) || slow.count(g + 1)) kept.push_back(cands[c]);
+        }
+        cands.swap(kept);
+      }
       std::unique_ptr<Plan> rbest;
       double rt = tb;
       for (size_t c = 1; c < cands.size(); ++c) {
