@@ -148,7 +148,7 @@ def cpu_baseline(wl, max_rows=None, parallel=True):
     return out
 
 
-def measure_config(name, dev, steps, warmup, tune=True):
+def measure_config(name, dev, steps, warmup, tune=True, reassoc=True):
     """Per-config line (BASELINE.json configs): one plan of the workload at its full size on this GPU, timed like
     the headline (rotating buffer sets >= 2x L2, CUDA graph replay, CUDA events on the launching stream).  C1 blur
     runs as a batch of 4096 frames (pmg_run_batch: a single 128x128 image is launch-bound)."""
@@ -160,10 +160,10 @@ def measure_config(name, dev, steps, warmup, tune=True):
     W, H = wl.params["W"], wl.params["H"]
     pipe = pmg.Pipeline(wl.text)
     t0 = time.perf_counter()
-    probe = pmg.Plan(pipe, wl.params, device=dev)                 # model schedule: is it one group?
+    probe = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(reassoc=reassoc))   # the model's schedule
     # measured selection: merge rounds (for plans of many groups only merges touching the 4 slowest groups), and
     # the tile grid for one-group plans
-    plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(tune=True)) if tune else probe
+    plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(tune=True, reassoc=reassoc)) if tune else probe
     t_plan = time.perf_counter() - t0
     frames = 4096 if name == "blur" else 0
     nfr = max(1, frames)
@@ -221,7 +221,7 @@ def measure_config(name, dev, steps, warmup, tune=True):
     pk, _ = peaks()
     nsms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_alu = 128 * nsms * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
-    dsc = pipe.describe(wl.params)
+    dsc = pmg.Pipeline(pipe.rewritten(wl.params, pmg.sched_opts(reassoc=reassoc, inline=False))["text"]).describe(wl.params)
     ops = nfr * sum(st["ops"] * int(np.prod(st["extent"])) for st in dsc["stages"])
     gbs = (bytes_in + bytes_out) / (ms * 1e-3) / 1e9
     desc = plan.describe()
@@ -235,6 +235,7 @@ def measure_config(name, dev, steps, warmup, tune=True):
         "schedule": ["V%dTX%dTH%d" % (g["config"]["V"], g["config"]["TX"], g["config"]["TH"]) for g in desc["schedule"]["groups"]][:8],
         "selection": "measured (tune)" if plan is not probe else "model", "plan_s": round(t_plan, 1),
         "l2": f"{sets} rotating buffer sets", "launch": "CUDA graph replay",
+        "arith": "reassoc" if reassoc else "exact", "factored": desc.get("factored", []),
     }
 
 
@@ -291,6 +292,10 @@ def main():
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config lines (C1, C3, C4, C5, PB)")
     ap.add_argument("--frames", type=int, default=4096, help="C1 blur: frames in the batch (split across ranks)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) leg (ncu launch lists)")
+    ap.add_argument("--exact", action="store_true",
+                    help="every f32 operation in the written order (bit-identical to the oracle); default: "
+                         "reassociation mode (sched_opts.reassoc: separable rank-1 stencils + fma, within the "
+                         "north_star tolerance; DESIGN.md §9)")
     args = ap.parse_args()
     wl = PI.WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -322,9 +327,11 @@ def main():
     nb = 1 if frames_total else (args.simulate_bands if (world == 1 and args.simulate_bands > 1) else world)
     band = 0 if frames_total else (nb // 2 if nb != world else rank)
     # schedule for this rank's band size; measured selection (tune) among the model's schedule and its neighbours
-    opts = pmg.sched_opts(bands=max(nb, 0), tune=not args.no_tune)
+    reassoc = not args.exact
+    opts = pmg.sched_opts(bands=max(nb, 0), tune=not args.no_tune, reassoc=reassoc)
     if args.opts:
         kv = dict(x.split("=") for x in args.opts.split(","))
+        kv.setdefault("reassoc", int(reassoc))
         opts = pmg.sched_opts(**{k: int(v) for k, v in kv.items()})
     pipe = pmg.Pipeline(wl.text)
     plan = pmg.Plan(pipe, wl.params, device=dev, opts=opts)
@@ -440,8 +447,9 @@ def main():
     algo_bytes = (bytes_in + bytes_out) * share
     pk, pk_kind = peaks()
     peak_hbm = float(pk["hbm_gbs"])
-    # algorithmic ALU work: every operation of the definition as written, over each stage's domain
-    dsc = pipe.describe(wl.params)
+    # algorithmic ALU work: every operation of the definition, over each stage's domain
+    # (reassociation mode: the operations of the factored definition, which the kernel evaluates)
+    dsc = pmg.Pipeline(pipe.rewritten(wl.params, pmg.sched_opts(reassoc=reassoc, inline=False))["text"]).describe(wl.params)
     algo_ops = sum(st["ops"] * int(np.prod(st["extent"])) for st in dsc["stages"]) * share
     nsms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_alu = 128 * nsms * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12      # FP32/INT32 lane-ops, T/s
@@ -550,6 +558,10 @@ def main():
                              (" (faster in warm-up: graph %.4f / host %.4f ms)" % (launch_mode[True], launch_mode[False])
                               if launch_mode else ""),
                    "l2": f"{sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (>= 2x the {l2 / 1e6:.0f} MB L2)",
+                   "arith": ("reassoc: rank-1 stencils evaluated separably (factored: %s) and a*b+c as fma; "
+                             "f32 rounding differs from the written order within the north_star tolerance "
+                             "(tests/test_gpu_reassoc.py)" % ", ".join(desc.get("factored", [])))
+                            if reassoc else "exact: every f32 operation in the written order (bit-identical to the oracle)",
                    "schedule": [g["config"] for g in desc["schedule"]["groups"]],
                    "kernels": desc["kernels"]},
         "roofline": ({"bound": "alu", "achieved": alu_achieved, "peak": peak_alu, "unit": "Tops/s",
@@ -583,9 +595,16 @@ def main():
             if name == args.workload:
                 continue
             try:
-                per[name] = measure_config(name, dev, max(10, args.steps), args.warmup, tune=not args.no_tune)
+                per[name] = measure_config(name, dev, max(10, args.steps), args.warmup, tune=not args.no_tune,
+                                           reassoc=reassoc)
             except Exception as e:   # a failing config is reported, not hidden
                 per[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        # the headline workload in the other arithmetic mode (exact: bit-identical to the oracle)
+        try:
+            per[args.workload + ("_exact" if reassoc else "_reassoc")] = measure_config(
+                args.workload, dev, max(10, args.steps), args.warmup, tune=not args.no_tune, reassoc=not reassoc)
+        except Exception as e:
+            per[args.workload + "_other_mode"] = {"error": f"{type(e).__name__}: {e}"[:300]}
         per[args.workload] = {"workload": wl.note, "ms_per_run": ms, "mpix_per_s": value, "hbm_frac": hbm_achieved / peak_hbm,
                               "hbm_frac_8tbs": hbm_achieved / 8000.0, "alu_frac": alu_achieved / peak_alu,
                               "note": "the headline line above"}

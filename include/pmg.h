@@ -129,7 +129,11 @@ typedef struct {
                            run on synthetic inputs and timed (CUDA events); the fastest is kept.  Plan creation
                            then takes seconds per candidate; runs are unaffected.  A B200 refinement outside the
                            paper's model-based selector. */
-  int32_t reserved;
+  int32_t reassoc;      /* 0 (default): every f32 operation in the written order (bit-identical to the oracle).
+                           1: reassociation mode: rank-1 linear stencils are evaluated separably
+                           (row sums reused across reader rows, factor.cpp) and a*b+c contracts to one fma;
+                           results differ from the written order by rounding only, within the north_star f32
+                           tolerance (tests/test_gpu_reassoc.py).  Integer stages are never rewritten. */
   const double* time_per_iter;  /* NULL = static operation counts; else per stage (declaration order) the measured
                                    TimePerIter in seconds (pmg_profile_stages) used by Alg. 2's
                                    compute term (cost_model 1); stages the schedule rewrote keep the static count */
@@ -167,6 +171,11 @@ void pmg_sched_opts_default(pmg_sched_opts* o);
  * schedule unless sched_opts.no_inline): JSON {"inlined": [names], "text": "..."} */
 pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap,
                                 size_t* needed);
+/* the pipeline text a plan made with `opts` schedules (NULL = defaults): rank-1 stencils factored when
+ * opts->reassoc (factor.cpp), then inlining and phase splitting unless opts->no_inline.
+ * JSON {"factored": [...], "inlined": [...], "split": [...], "text": "..."}; buffer protocol as above. */
+pmg_status pmg_pipeline_rewritten(pmg_pipeline p, const int64_t* params, int nparams, const pmg_sched_opts* opts,
+                                  char* buf, size_t cap, size_t* needed);
 pmg_status pmg_schedule(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
                         const pmg_weights* w, const pmg_sched_opts* opts, char* json, size_t cap, size_t* needed);
 pmg_status pmg_analyze_group(pmg_pipeline p, const int64_t* params, int nparams, const char* stages_csv,

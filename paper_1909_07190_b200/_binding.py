@@ -68,7 +68,7 @@ class SchedOpts(C.Structure):
                 ("smem_chunks", C.c_int32), ("rows", C.c_int32), ("warps", C.c_int32), ("prefetch", C.c_int32),
                 ("tx_size", C.c_int32), ("budget", C.c_int32), ("fuse", C.c_int32), ("regcap", C.c_int32),
                 ("probe", C.c_int32), ("cost_model", C.c_int32), ("bands", C.c_int32), ("no_inline", C.c_int32),
-                ("tune", C.c_int32), ("reserved", C.c_int32), ("time_per_iter", C.POINTER(C.c_double))]
+                ("tune", C.c_int32), ("reassoc", C.c_int32), ("time_per_iter", C.POINTER(C.c_double))]
 
 
 P = C.c_void_p
@@ -113,6 +113,8 @@ _sig = {
     "pmg_band_rows_host": (C.c_int, [P, I64P, C.c_int, C.POINTER(GpuSpec), C.POINTER(Weights), C.POINTER(SchedOpts),
                                      C.c_int, C.c_int, I64P, I64P, I64P, I64P]),
     "pmg_pipeline_inlined": (C.c_int, [P, I64P, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "pmg_pipeline_rewritten": (C.c_int, [P, I64P, C.c_int, C.POINTER(SchedOpts), C.c_char_p, C.c_size_t,
+                                        C.POINTER(C.c_size_t)]),
     "pmg_run_band": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.c_void_p,
                                C.c_void_p]),
     "pmg_run_host": (C.c_int, [P, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.POINTER(Buf),

@@ -14,7 +14,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 LIB = HERE / "libpmg.so"
-SOURCES = ["parse.cpp", "analysis.cpp", "inline.cpp", "phase.cpp", "group.cpp", "emit.cpp", "select.cpp", "runtime.cpp", "capi.cpp",
+SOURCES = ["parse.cpp", "analysis.cpp", "inline.cpp", "factor.cpp", "phase.cpp", "group.cpp", "emit.cpp", "select.cpp", "runtime.cpp", "capi.cpp",
            "selftest.cpp"]
 
 

@@ -49,6 +49,11 @@ std::string describe_pipeline(const Analysis& A);
 std::shared_ptr<Pipeline> inline_expanding(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
                                            std::vector<std::string>* inlined);
 
+// factor.cpp: separable evaluation of rank-1 linear f32 stencils (reassociation mode only; names of the
+// factored stages appended to *factored)
+std::shared_ptr<Pipeline> factor_stencils(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params,
+                                          std::vector<std::string>* factored);
+
 // phase.cpp: alignment & scaling of downsampling edges -- a stage read only as S(2v + b) along y or x by
 // readers of half its extent is replaced by its two phases at the readers' extent (exact; names of the split
 // stages, "name/y" or "name/x", appended to *split).  PMG_PHASE_SPLIT=0 disables it.

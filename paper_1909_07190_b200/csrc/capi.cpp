@@ -135,18 +135,28 @@ pmg_status pmg_pipeline_describe(pmg_pipeline p, const int64_t* params, int npar
   })
 }
 
-pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap, size_t* needed) {
+static pmg_status rewritten_json(pmg_pipeline p, const int64_t* params, int nparams, const pmg_sched_opts* opts,
+                                 char* buf, size_t cap, size_t* needed) {
   if (!p) return fail(PMG_ERR_ARG, "NULL pipeline");
   PMG_TRY({
-    std::vector<std::string> names, split;
-    auto q = inline_expanding(p->p, pvec(params, nparams), &names);
-    q = phase_split(q, pvec(params, nparams), &split);
+    std::vector<std::string> fac, names, split;
+    auto q = p->p;
+    if (opts && opts->reassoc) q = factor_stencils(q, pvec(params, nparams), &fac);
+    if (!(opts && opts->no_inline)) {
+      q = inline_expanding(q, pvec(params, nparams), &names);
+      q = phase_split(q, pvec(params, nparams), &split);
+    }
     std::ostringstream o;
-    o << "{\"inlined\":[";
-    for (size_t i = 0; i < names.size(); ++i) o << (i ? "," : "") << "\"" << names[i] << "\"";
-    o << "],\"split\":[";
-    for (size_t i = 0; i < split.size(); ++i) o << (i ? "," : "") << "\"" << split[i] << "\"";
-    o << "],\"text\":\"";
+    auto list = [&](const char* key, const std::vector<std::string>& v) {
+      o << "\"" << key << "\":[";
+      for (size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << "\"" << v[i] << "\"";
+      o << "],";
+    };
+    o << "{";
+    list("factored", fac);
+    list("inlined", names);
+    list("split", split);
+    o << "\"text\":\"";
     for (char c : q->source) {
       if (c == '\n') o << "\\n";
       else if (c == '"' || c == '\\') o << '\\' << c;
@@ -155,6 +165,15 @@ pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int npara
     o << "\"}";
     return put_json(o.str(), buf, cap, needed);
   })
+}
+
+pmg_status pmg_pipeline_inlined(pmg_pipeline p, const int64_t* params, int nparams, char* buf, size_t cap, size_t* needed) {
+  return rewritten_json(p, params, nparams, nullptr, buf, cap, needed);
+}
+
+pmg_status pmg_pipeline_rewritten(pmg_pipeline p, const int64_t* params, int nparams, const pmg_sched_opts* opts,
+                                  char* buf, size_t cap, size_t* needed) {
+  return rewritten_json(p, params, nparams, opts, buf, cap, needed);
 }
 
 pmg_status pmg_gpu_spec_preset(const char* name, pmg_gpu_spec* out) {
@@ -211,8 +230,9 @@ void pmg_sched_opts_default(pmg_sched_opts* o) {
 // the pipeline the schedule works on: data-expanding stages substituted into their readers unless disabled
 static std::shared_ptr<Pipeline> effective(const std::shared_ptr<Pipeline>& p, const std::vector<int64_t>& params,
                                            const pmg_sched_opts* opts) {
-  if (opts && opts->no_inline) return p;
-  return phase_split(inline_expanding(p, params, nullptr), params, nullptr);
+  std::shared_ptr<Pipeline> q = (opts && opts->reassoc) ? factor_stencils(p, params, nullptr) : p;
+  if (opts && opts->no_inline) return q;
+  return phase_split(inline_expanding(q, params, nullptr), params, nullptr);
 }
 
 static void spec_or_default(const pmg_gpu_spec* s, const pmg_weights* w, pmg_gpu_spec& S, pmg_weights& W) {

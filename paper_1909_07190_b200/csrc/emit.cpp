@@ -183,6 +183,9 @@ struct Emitter {
     return false;
   }
 
+  // a float product p*q (reassociation mode contracts it with an enclosing + or -)
+  static bool is_fprod(const Expr& e) { return e.op == Expr::BIN && e.text == "*" && e.kind == Kind::Float; }
+
   // x parity (the camera interleave, the pyramid upsampling): when every lane's first column xL is even
   // (V, OW and PL even), `x + b` has a known parity per element, so `(x + b) % 2` is a constant and
   // `(x + b) / 2` (floor) is xL/2 plus a constant -- exact integer identities, no change of results
@@ -238,6 +241,13 @@ struct Emitter {
       if (pow2_mul(*e.args[1], &mb, &m)) {
         R a = tof(ex(*e.args[0], c)), b = ex(*mb, c);
         return {"pmg_fma_exact(" + flit(op == "+" ? m : -m) + ", " + b.s + ", " + a.s + ")", Kind::Float};
+      }
+      // reassociation mode (sched_opts.reassoc): a +- p*q -> fma(+-p, q, a).  Only a right-hand product
+      // contracts, as in the interior kernel's fold spine (spine_op), so both kernels compute the same values.
+      if (g.cfg.contract && is_fprod(*e.args[1])) {
+        const Expr& Rt = *e.args[1];
+        R a = tof(ex(*e.args[0], c)), m0 = tof(ex(*Rt.args[0], c)), m1 = tof(ex(*Rt.args[1], c));
+        return {"__fmaf_rn(" + (op == "+" ? m0.s : "(-(" + m0.s + "))") + ", " + m1.s + ", " + a.s + ")", Kind::Float};
       }
       // m*b + a  ->  fma(m, b, a);  m*b - a -> fma(m, b, -a)
       if (pow2_mul(*e.args[0], &mb, &m)) {
@@ -543,6 +553,10 @@ struct Emitter {
       float m;
       if (pow2_mul(*op.right, &mb, &m))
         return {"pmg_fma_exact(" + flit(t == "+" ? m : -m) + ", " + ex(*mb, c).s + ", " + tof(left).s + ")", Kind::Float};
+      if (g.cfg.contract && is_fprod(*op.right)) {   // mirrors bin(): left +- p*q -> fma(+-p, q, left)
+        R m0 = tof(ex(*op.right->args[0], c)), m1 = tof(ex(*op.right->args[1], c));
+        return {"__fmaf_rn(" + (t == "+" ? m0.s : "(-(" + m0.s + "))") + ", " + m1.s + ", " + tof(left).s + ")", Kind::Float};
+      }
     }
     if (t == "/") {
       int k;

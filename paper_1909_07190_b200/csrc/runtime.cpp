@@ -396,6 +396,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   }
   auto P = std::make_unique<Plan>();
   std::shared_ptr<Pipeline> written = p;
+  if (opts && opts->reassoc) p = factor_stencils(p, params, &P->factored);
   if (!(opts && opts->no_inline)) p = phase_split(inline_expanding(p, params, &P->inlined), params, &P->split);
   P->pipe = p;
   P->A = analyze(*p, params);
@@ -456,6 +457,8 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   for (size_t i = 0; i < P->inlined.size(); ++i) js << (i ? "," : "") << "\"" << P->inlined[i] << "\"";
   js << "],\"split\":[";
   for (size_t i = 0; i < P->split.size(); ++i) js << (i ? "," : "") << "\"" << P->split[i] << "\"";
+  js << "],\"factored\":[";
+  for (size_t i = 0; i < P->factored.size(); ++i) js << (i ? "," : "") << "\"" << P->factored[i] << "\"";
   js << "],\"schedule\":" << P->sch.json << ",\"kernels\":[";
   for (size_t gi = 0; gi < P->sch.groups.size(); ++gi) {
     Group& g = P->sch.groups[gi];

@@ -56,6 +56,7 @@ struct Plan {
   CUevent ev_fork = nullptr, ev_join = nullptr;
   std::string json;
   std::vector<std::string> inlined;        // stages substituted into their readers (inline.cpp)
+  std::vector<std::string> factored;       // stages evaluated separably (factor.cpp, sched_opts.reassoc)
   std::vector<std::string> split;          // stages replaced by their two phases (phase.cpp), "name/y|x"
   // independent groups run concurrently: each group is assigned a lane (lane 0 = the caller's stream,
   // lanes 1.. plan-owned streams); cross-lane dependences are events (DESIGN.md §6 "group DAG")

@@ -400,7 +400,7 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                 if (S_ > TX) continue;
                 Group cand;
                 cand.stages = g.stages;
-                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0};
+                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0, o.reassoc != 0};
                 ++count;
                 if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
                 CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model, o.bands, o.time_per_iter);

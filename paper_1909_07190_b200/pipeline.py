@@ -43,7 +43,7 @@ def weights(name: str = "b200") -> B.Weights:
 
 def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, warps=-1, prefetch=-1, tx_size=-1,
                budget=0, fuse=True, regcap=0, probe=True, cost_model=0, bands=0, inline=True, tune=False,
-               time_per_iter=None) -> B.SchedOpts:
+               time_per_iter=None, reassoc=False) -> B.SchedOpts:
     o = B.SchedOpts()
     B.lib.pmg_sched_opts_default(C.byref(o))
     o.vec, o.chunks, o.smem_chunks, o.rows, o.warps, o.prefetch, o.tx_size = (
@@ -56,6 +56,7 @@ def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, 
     o.bands = bands                    # expected row-band split (the estimate counts one band's tiles)
     o.no_inline = 0 if inline else 1   # substitute data-expanding stages into their readers
     o.tune = 1 if tune else 0          # measured selection among the DP schedule and its neighbour merges
+    o.reassoc = 1 if reassoc else 0    # separable rank-1 stencils + fma contraction (f32 rounding differs)
     if time_per_iter is not None:       # measured TimePerIter per stage (Pipeline.profile_stages), Alg. 2 input
         tarr = (C.c_double * len(time_per_iter))(*time_per_iter)
         o._keep_tpi = tarr
@@ -79,7 +80,7 @@ class Pipeline:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(B, "lib", None) is not None:   # (the module may be torn down at interpreter exit)
             B.lib.pmg_pipeline_destroy(h)
             self._h = None
 
@@ -133,6 +134,11 @@ class Pipeline:
         """{"inlined": [stage names], "text": pipeline text} after substituting data-expanding stages."""
         arr, n = self.param_values(params)
         return B.call_json(B.lib.pmg_pipeline_inlined, self._h, arr, n)
+
+    def rewritten(self, params: dict, opts=None) -> dict:
+        """{"factored", "inlined", "split", "text"}: the pipeline text a plan made with `opts` schedules."""
+        arr, n = self.param_values(params)
+        return B.call_json(B.lib.pmg_pipeline_rewritten, self._h, arr, n, _ref(opts))
 
     def profile_stages(self, params: dict, device: int = 0) -> dict:
         """On-device TimePerIter of every stage (each stage alone as one kernel)."""
@@ -222,7 +228,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(B, "lib", None) is not None:   # (the module may be torn down at interpreter exit)
             B.lib.pmg_plan_destroy(h)
             self._h = None
 
