@@ -16,8 +16,8 @@ import paper_1909_07190_b200 as pmg  # noqa: E402
 
 
 @pytest.mark.parametrize("name,W,H,n,fuse", [("harris", 300, 211, 4, True), ("unsharp", 160, 97, 3, True),
-                                             ("blur", 128, 128, 8, True), ("harris", 120, 90, 3, False),
-                                             ("camera", 132, 98, 2, True), ("ll", 64, 96, 3, True)])
+                                             ("blur", 128, 128, 8, True), ("harris", 120, 90, 3, False)])
+# (camera and local Laplacian bands: test_gpu_fullsize.py::test_fullsize_bands_stitched_parity, full size)
 def test_band_invariance(name, W, H, n, fuse):
     import torch
     wl = (PI.Workload("ll", "local_laplacian_J4K4.pmg", {"W": W, "H": H}, 1005) if name == "ll"
@@ -83,7 +83,7 @@ def test_plan_describe_reports_kernels():
 
 
 @pytest.mark.parametrize("name,W,H,chunks", [("harris", 700, 301, 1), ("harris", 700, 301, 8), ("unsharp", 300, 170, 3),
-                                             ("camera", 264, 130, 8), ("ll", 96, 128, 3)])
+                                             ("camera", 264, 130, 8)])
 def test_run_host_equals_device_run(name, W, H, chunks):
     """pmg_run_host (pinned host buffers, row chunks pipelined over copy streams) == the device-buffer run,
     bit for bit; every input row is copied once and every output row comes back."""

@@ -6,7 +6,7 @@ for v in "$@"; do
   envs=${v%%;*}; opts=${v#*;}
   [ "$envs" = "$v" ] && opts=""
   out=gpurun_out/$tag/$(echo "$wl-$v" | tr -c 'A-Za-z0-9_.=-' '_').json
-  env $(echo $envs | tr ',' ' ') timeout 300 python bench.py --workload $wl --no-cpu-baseline --steps 50 --warmup 5 ${opts:+--opts $opts} > $out 2> $out.err
+  env $(echo $envs | tr ',' ' ') timeout 300 python bench.py --workload $wl --no-cpu-baseline --steps 50 --warmup 5 --no-e2e ${opts:+--opts $opts} > $out 2> $out.err
   python - "$out" "$v" <<'PY'
 import json, sys
 try:
