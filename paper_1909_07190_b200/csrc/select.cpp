@@ -23,6 +23,7 @@
 #include <functional>
 #include <limits>
 #include <map>
+#include <set>
 #include <sstream>
 #include <tuple>
 
@@ -470,11 +471,34 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
     for (size_t i = 0; i < s.groups.size(); ++i) s.groups[i].name = "pmg_g" + std::to_string(i);
   };
   if (o.group_of_stage) {
-    // explicit grouping: one group per distinct index, ordered by first topological occurrence
+    // explicit grouping: one group per distinct index, in a topological order of the group DAG (ties: first
+    // occurrence in p.topo); a grouping whose groups depend on each other cyclically is rejected
     std::vector<int> gos(o.group_of_stage, o.group_of_stage + n);
-    std::vector<int> seen;
+    std::vector<int> labels;
     for (int s : p.topo)
-      if (std::find(seen.begin(), seen.end(), gos[s]) == seen.end()) seen.push_back(gos[s]);
+      if (std::find(labels.begin(), labels.end(), gos[s]) == labels.end()) labels.push_back(gos[s]);
+    std::vector<int> seen;
+    {
+      const size_t L = labels.size();
+      auto li = [&](int lab) { return (int)(std::find(labels.begin(), labels.end(), lab) - labels.begin()); };
+      std::vector<std::set<int>> preds(L);
+      for (int s = 0; s < n; ++s)
+        for (int q : p.producers[s])
+          if (gos[q] != gos[s]) preds[li(gos[s])].insert(li(gos[q]));
+      std::vector<bool> done(L, false);
+      for (size_t k = 0; k < L; ++k) {
+        int pick = -1;
+        for (size_t c = 0; c < L && pick < 0; ++c) {
+          if (done[c]) continue;
+          bool ok = true;
+          for (int q : preds[c]) ok = ok && done[q];
+          if (ok) pick = (int)c;
+        }
+        if (pick < 0) throw Error(PMG_ERR_INFEASIBLE, "explicit grouping: groups depend on each other cyclically");
+        done[pick] = true;
+        seen.push_back(labels[pick]);
+      }
+    }
     sch.group_of_stage = gos;
     std::ostringstream js;
     double total = 0;
@@ -496,43 +520,92 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
     name_groups(sch);
     return sch;
   }
-  // DP over contiguous runs of the topological order (each run is convex): best[j] = min_i best[i] + cost(i..j)
+  // DP over contiguous runs of a topological order (each run is convex): best[j] = min_i best[i] + cost(i..j).
+  // Two orders are tried -- producers as early as possible (p.topo: declaration order among ready stages) and
+  // as late as possible (ALAP: each stage right before its first consumer; a pyramid's per-level output
+  // stages then sit next to the same-extent stage that consumes them, e.g. the local Laplacian's outLP_j and
+  // outG_j) -- and the order with the smaller DP cost is kept.
   const double INF = std::numeric_limits<double>::infinity();
-  std::vector<double> best(n + 1, INF);
-  std::vector<int> from(n + 1, -1);
-  std::vector<std::vector<Group>> seg_group(n + 1, std::vector<Group>(n + 1));
-  std::vector<std::vector<double>> seg_cost(n + 1, std::vector<double>(n + 1, INF));
-  std::vector<std::vector<CostBreakdown>> seg_cb(n + 1, std::vector<CostBreakdown>(n + 1));
-  best[0] = 0;
-  const bool fuse = o.fuse != 0;
-  for (int j = 1; j <= n; ++j) {
-    for (int i = j - 1; i >= 0; --i) {
-      if (!fuse && j - i > 1) break;
-      if (best[i] == INF) continue;
-      std::vector<int> seg(p.topo.begin() + i, p.topo.begin() + j);
-      if (!feasible_stage_set(A, seg)) continue;
-      // grouping vector: stages of seg in group 0, every other stage in its own group
-      std::vector<int> gos(n);
-      for (int s = 0; s < n; ++s) gos[s] = s + 1;
-      for (int s : seg) gos[s] = 0;
-      Group g;
-      g.stages = seg;
-      CostBreakdown cb;
-      if (!best_config(A, g, gos, S, w, o, &cb)) continue;
-      seg_group[i][j] = g;
-      seg_cost[i][j] = cb.cost;
-      seg_cb[i][j] = cb;
-      if (best[i] + cb.cost < best[j]) { best[j] = best[i] + cb.cost; from[j] = i; }
+  std::vector<int> alap;
+  {
+    std::vector<int> rem(n);
+    for (int s = 0; s < n; ++s) rem[s] = (int)p.consumers[s].size();
+    std::set<int> ready;
+    for (int s = 0; s < n; ++s)
+      if (!rem[s]) ready.insert(s);
+    while (!ready.empty()) {
+      // from the end: a ready stage of the extent just placed first (it can join that stage's group), else the
+      // latest declaration
+      int s = *ready.rbegin();
+      if (!alap.empty())
+        for (auto it = ready.rbegin(); it != ready.rend(); ++it)
+          if (A.stage_ext[*it] == A.stage_ext[alap.back()] || (A.stage_ext[*it].e[1] == A.stage_ext[alap.back()].e[1] &&
+                                                               A.stage_ext[*it].e[2] == A.stage_ext[alap.back()].e[2])) {
+            s = *it;
+            break;
+          }
+      ready.erase(s);
+      alap.push_back(s);
+      for (int q : p.producers[s])
+        if (--rem[q] == 0) ready.insert(q);
     }
-    if (best[j] == INF) throw Error(PMG_ERR_INFEASIBLE, "no feasible group ends at stage " + p.stages[p.topo[j - 1]].name);
+    std::reverse(alap.begin(), alap.end());
   }
+  const bool fuse = o.fuse != 0;
+  struct DP {
+    std::vector<double> best;
+    std::vector<int> from;
+    std::vector<std::vector<Group>> seg_group;
+  };
+  auto run_dp = [&](const std::vector<int>& ord) {
+    DP d;
+    d.best.assign(n + 1, INF);
+    d.from.assign(n + 1, -1);
+    d.seg_group.assign(n + 1, std::vector<Group>(n + 1));
+    d.best[0] = 0;
+    for (int j = 1; j <= n; ++j) {
+      for (int i = j - 1; i >= 0; --i) {
+        if (!fuse && j - i > 1) break;
+        if (d.best[i] == INF) continue;
+        std::vector<int> seg(ord.begin() + i, ord.begin() + j);
+        if (!feasible_stage_set(A, seg)) continue;
+        // grouping vector: stages of seg in group 0, every other stage in its own group
+        std::vector<int> gos(n);
+        for (int s = 0; s < n; ++s) gos[s] = s + 1;
+        for (int s : seg) gos[s] = 0;
+        Group g;
+        g.stages = seg;
+        CostBreakdown cb;
+        if (!best_config(A, g, gos, S, w, o, &cb)) continue;
+        d.seg_group[i][j] = g;
+        if (d.best[i] + cb.cost < d.best[j]) { d.best[j] = d.best[i] + cb.cost; d.from[j] = i; }
+      }
+      if (d.best[j] == INF) throw Error(PMG_ERR_INFEASIBLE, "no feasible group ends at stage " + p.stages[ord[j - 1]].name);
+    }
+    return d;
+  };
+  DP dp = run_dp(p.topo);
+  std::vector<int> topo = p.topo;
+  bool late = false;
+  const char* ord_env = getenv("PMG_ORDER");   // experiment knob: "asap" / "alap" forces one order
+  if (alap != p.topo && fuse && !(ord_env && std::strcmp(ord_env, "asap") == 0)) {
+    DP d2 = run_dp(alap);
+    if (d2.best[n] < dp.best[n] - 1e-9 || (ord_env && std::strcmp(ord_env, "alap") == 0)) {
+      dp = std::move(d2);
+      topo = alap;
+      late = true;
+    }
+  }
+  std::vector<double>& best = dp.best;
+  std::vector<int>& from = dp.from;
+  std::vector<std::vector<Group>>& seg_group = dp.seg_group;
   std::vector<std::pair<int, int>> segs;
   for (int j = n; j > 0; j = from[j]) segs.push_back({from[j], j});
   std::reverse(segs.begin(), segs.end());
   auto gos_of = [&](const std::vector<std::pair<int, int>>& sg) {
     std::vector<int> v(n, -1);
     for (size_t gi = 0; gi < sg.size(); ++gi)
-      for (int q = sg[gi].first; q < sg[gi].second; ++q) v[p.topo[q]] = (int)gi;
+      for (int q = sg[gi].first; q < sg[gi].second; ++q) v[topo[q]] = (int)gi;
     return v;
   };
   // probed merge pass: the DP costs segments with the register *estimate*, which over-estimates large fused
@@ -544,7 +617,7 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
       total = 0;
       for (auto& q : sg) {
         Group h;
-        h.stages.assign(p.topo.begin() + q.first, p.topo.begin() + q.second);
+        h.stages.assign(topo.begin() + q.first, topo.begin() + q.second);
         CostBreakdown cb;
         if (!best_config(A, h, gv, S, w, o, &cb, probe) || cb.infinite) return false;
         total += cb.cost;
@@ -556,7 +629,7 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
       for (bool changed = true; changed && segs.size() > 1;) {
         changed = false;
         for (size_t gi = 0; gi + 1 < segs.size(); ++gi) {
-          std::vector<int> merged(p.topo.begin() + segs[gi].first, p.topo.begin() + segs[gi + 1].second);
+          std::vector<int> merged(topo.begin() + segs[gi].first, topo.begin() + segs[gi + 1].second);
           if (!feasible_stage_set(A, merged)) continue;
           auto trial = segs;
           trial[gi].second = trial[gi + 1].second;
@@ -574,7 +647,7 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
   }
   sch.group_of_stage = gos_of(segs);
   std::ostringstream js;
-  js << "{\"mode\":\"dp\",\"dp_cost\":" << best[n] << ",\"groups\":[";
+  js << "{\"mode\":\"dp\",\"order\":\"" << (late ? "alap" : "asap") << "\",\"dp_cost\":" << best[n] << ",\"groups\":[";
   for (size_t gi = 0; gi < segs.size(); ++gi) {
     Group g = seg_group[segs[gi].first][segs[gi].second];
     // re-select with the final grouping (materialisation depends on the other groups) and with the
