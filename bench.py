@@ -292,6 +292,10 @@ def main():
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config lines (C1, C3, C4, C5, PB)")
     ap.add_argument("--frames", type=int, default=4096, help="C1 blur: frames in the batch (split across ranks)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) leg (ncu launch lists)")
+    ap.add_argument("--exchange", action="store_true",
+                    help="row bands in halo-exchange mode (SURVEY NEXT-2): each band computes its own rows of every "
+                         "group and receives halo rows after the producing group (NCCL send/recv at N>1; with "
+                         "--simulate-bands the received rows are device copies from a second workspace)")
     ap.add_argument("--exact", action="store_true",
                     help="every f32 operation in the written order (bit-identical to the oracle); default: "
                          "reassociation mode (sched_opts.reassoc: separable rank-1 stencils + fma, within the "
@@ -341,6 +345,8 @@ def main():
 
     from gpu_util_bench import device_inputs
     o_r0, o_r1, i_r0, i_r1 = plan.band_rows(band, nb)
+    if args.exchange and nb > 1 and not frames_total:
+        i_r0, i_r1 = plan.band_exchange(band, nb)["in"]     # own rows + the input halo of the band's groups
     all_bands = [plan.band_rows(b, nb)[:2] for b in range(nb)]
     # rotating buffer sets: together at least 2x L2, so no run finds its inputs in L2 (bands are small at N>1)
     set_bytes = sum(int(np.prod(io.shape[:-2])) * (i_r1 - i_r0) * io.shape[-1] * pmg._binding.DTYPE_SIZE[io.dtype]
@@ -365,10 +371,31 @@ def main():
         out_sets.append(outs)
     ws = plan.workspace(max(1, nf))
 
+    xchg = args.exchange and nb > 1 and not frames_total
+    if xchg:
+        from paper_1909_07190_b200.dist import exchange_groups, exchange_points, rows_view, run_band_exchange
+        xgeoms = [plan.band_exchange(b, nb) for b in range(nb)]
+        xpts = exchange_points(xgeoms)
+        xgeom = xgeoms[band]
+        ws_peer = torch.zeros_like(ws)
+        xruns = exchange_groups({"groups": xgeom["groups"], "send": [{"after_group": a} for a in xpts], "recv": []})
+
     def launch(i, st):
         ins, outs = in_sets[i % sets], out_sets[i % sets]
         if frames_total:
             plan.run_batch(ins, outs, ws, st)
+        elif xchg and world > 1:
+            run_band_exchange(plan, band, nb, ins, outs, ws, st, points=xpts)
+        elif xchg:
+            # one GPU: this band's groups, and after each producing group its received rows as device copies
+            # (from a second workspace standing in for the peers' memory)
+            with torch.cuda.stream(st):
+                for g0, g1 in xruns:
+                    plan.run_band_groups(band, nb, g0, g1, ins, outs, ws, st)
+                    for t in xgeom["recv"]:
+                        if t["after_group"] == g1 - 1:
+                            stg = xgeom["stages"][t["stage"]]
+                            rows_view(ws, stg, t["rows"]).copy_(rows_view(ws_peer, stg, t["rows"]), non_blocking=True)
         elif nb > 1:
             plan.run_band(band, nb, ins, outs, ws, st)
         else:
@@ -587,6 +614,11 @@ def main():
         line["config"]["parallelism"] = f"frames x{world}"
     if nb != world:
         line["config"]["simulated_bands"] = f"band {band} of {nb} timed on one GPU; value = whole image / band time"
+    if xchg:
+        line["config"]["band_mode"] = (f"halo exchange (SURVEY NEXT-2): own rows per group, {len(xpts)} exchange "
+                                       f"points, {len(xgeom['recv'])} received row blocks, input rows "
+                                       f"{i_r1 - i_r0} (recompute would need {plan.band_rows(band, nb)[3] - plan.band_rows(band, nb)[2]})"
+                                       + ("; received rows are device copies on one GPU" if world == 1 else "; NCCL send/recv"))
     if not args.no_cpu_baseline and world == 1 and nb == 1:
         line["cpu_baseline"] = cpu_baseline(wl)
     if not args.no_per_config and world == 1 and nb == 1 and not args.opts:

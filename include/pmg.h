@@ -221,6 +221,27 @@ pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams
 pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, int nin, const pmg_buf* out,
                         int nout, void* workspace, void* stream);
 
+/* ---- halo-exchange bands (the paper is single-GPU) ----
+ * Instead of recomputing the pipeline-wide cumulative halo, band b of n computes only its OWN rows of every
+ * group, own_g(b) = [b*Hg/n, (b+1)*Hg/n) at the group's row extent Hg, and receives the rows of earlier groups'
+ * workspace stages that its later groups read beyond them from the bands owning them (pyramid pipelines: a few
+ * rows per level instead of ~4x recompute at 8 bands).
+ * pmg_band_exchange: JSON {"band","nbands","in":[lo,hi] (image rows of the band's input buffers),"out":[lo,hi],
+ *   "groups":[[lo,hi] own rows per group],"stages":[{"name","group","offset","row_pitch","plane_pitch","planes",
+ *   "rows","buf":[lo,hi] (rows the band's workspace slot holds: row r of plane k is at workspace + offset +
+ *   k*plane_pitch + (r - buf.lo)*row_pitch),"need","own"}],"recv":[{"stage","peer","rows","after_group"}],
+ *   "send":[...]}; every rank derives the same pairs, so the caller's transport (NCCL send/recv, peer copies)
+ *   only moves bytes.  Buffer protocol as pmg_schedule.
+ * pmg_run_band_groups: launch groups [group_begin, group_end) of band b in this mode; in[] holds image rows
+ *   "in", out[] liveout rows "out"; the workspace slots must hold the received rows of the stages those groups
+ *   read (exchange after each group, before the next call).  Stream-ordered like pmg_run. */
+pmg_status pmg_band_exchange(pmg_plan plan, int band, int nbands, char* json, size_t cap, size_t* needed);
+pmg_status pmg_band_exchange_host(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                                  const pmg_weights* w, const pmg_sched_opts* opts, int band, int nbands, char* json,
+                                  size_t cap, size_t* needed);
+pmg_status pmg_run_band_groups(pmg_plan plan, int band, int nbands, int group_begin, int group_end, const pmg_buf* in,
+                               int nin, const pmg_buf* out, int nout, void* workspace, void* stream);
+
 /* end-to-end run from host memory (the bench's e2e path): host_in / host_out are host images in the
  * pmg_buf layout (pinned memory gives asynchronous copies); dev_in / dev_out are caller-owned full-size
  * device staging buffers (16-byte aligned pitches).  The image is cut into `chunks` row bands (1..64,

@@ -117,6 +117,11 @@ _sig = {
                                         C.POINTER(C.c_size_t)]),
     "pmg_run_band": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.c_void_p,
                                C.c_void_p]),
+    "pmg_band_exchange": (C.c_int, [P, C.c_int, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "pmg_band_exchange_host": (C.c_int, [P, I64P, C.c_int, C.POINTER(GpuSpec), C.POINTER(Weights), C.POINTER(SchedOpts),
+                                         C.c_int, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "pmg_run_band_groups": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf),
+                                      C.c_int, C.c_void_p, C.c_void_p]),
     "pmg_run_host": (C.c_int, [P, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.c_int, C.POINTER(Buf), C.POINTER(Buf),
                                C.c_void_p, C.c_int, C.c_void_p]),
     "pmg_selftest_shuffle": (C.c_int, [C.c_int, C.POINTER(C.c_int32)]),

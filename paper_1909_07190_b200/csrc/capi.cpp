@@ -471,6 +471,88 @@ pmg_status pmg_band_rows_host(pmg_pipeline p, const int64_t* params, int nparams
   })
 }
 
+// halo-exchange band geometry as JSON (one band's view; the sends / receives of every band pair are derived
+// from the same deterministic geometry on every rank)
+static std::string xchg_json(const Plan& P, int band, int nbands) {
+  const Pipeline& p = *P.pipe;
+  std::vector<BandXchg> all;
+  for (int b = 0; b < nbands; ++b) all.push_back(band_xchg(P, b, nbands));
+  const BandXchg& X = all[band];
+  std::vector<int> group_of(p.stages.size(), -1);
+  for (size_t gi = 0; gi < P.sch.groups.size(); ++gi)
+    for (int st : P.sch.groups[gi].stages) group_of[st] = (int)gi;
+  auto iv = [](RowIv r) { return "[" + std::to_string(r.lo) + "," + std::to_string(r.hi) + "]"; };
+  auto isect = [](RowIv a, RowIv b) { RowIv r{std::max(a.lo, b.lo), std::min(a.hi, b.hi)}; return r; };
+  std::ostringstream o;
+  o << "{\"band\":" << band << ",\"nbands\":" << nbands << ",\"in\":" << iv(X.in) << ",\"out\":" << iv(X.out)
+    << ",\"groups\":[";
+  for (size_t gi = 0; gi < X.own.size(); ++gi) o << (gi ? "," : "") << iv(X.own[gi]);
+  o << "],\"stages\":[";
+  std::ostringstream snd, rcv;
+  bool fs = true, fr = true;
+  for (size_t k = 0; k < P.ws.size(); ++k) {
+    const WsTensor& w = P.ws[k];
+    const int g = group_of[w.stage];
+    o << (k ? "," : "") << "{\"name\":\"" << p.stages[w.stage].name << "\",\"group\":" << g << ",\"offset\":" << w.offset
+      << ",\"row_pitch\":" << w.row_pitch << ",\"plane_pitch\":" << w.plane_pitch << ",\"planes\":" << w.planes
+      << ",\"rows\":" << w.rows << ",\"buf\":" << iv(X.buf[w.stage]) << ",\"need\":" << iv(X.need[w.stage])
+      << ",\"own\":" << iv(X.own[g]) << "}";
+    for (int c = 0; c < nbands; ++c) {
+      if (c == band) continue;
+      RowIv r = isect(all[c].own[g], X.need[w.stage]);     // rows band c owns that this band reads
+      if (r.hi > r.lo) {
+        rcv << (fr ? "" : ",") << "{\"stage\":" << k << ",\"peer\":" << c << ",\"rows\":" << iv(r) << ",\"after_group\":" << g << "}";
+        fr = false;
+      }
+      RowIv q = isect(X.own[g], all[c].need[w.stage]);     // rows this band owns that band c reads
+      if (q.hi > q.lo) {
+        snd << (fs ? "" : ",") << "{\"stage\":" << k << ",\"peer\":" << c << ",\"rows\":" << iv(q) << ",\"after_group\":" << g << "}";
+        fs = false;
+      }
+    }
+  }
+  o << "],\"recv\":[" << rcv.str() << "],\"send\":[" << snd.str() << "],\"workspace_bytes\":" << P.ws_bytes << "}";
+  return o.str();
+}
+
+pmg_status pmg_band_exchange(pmg_plan plan, int band, int nbands, char* json, size_t cap, size_t* needed) {
+  if (!plan || nbands < 1 || band < 0 || band >= nbands) return fail(PMG_ERR_ARG, "bad band");
+  PMG_TRY({ return put_json(xchg_json(*plan->plan, band, nbands), json, cap, needed); })
+}
+
+pmg_status pmg_band_exchange_host(pmg_pipeline p, const int64_t* params, int nparams, const pmg_gpu_spec* spec,
+                                  const pmg_weights* w, const pmg_sched_opts* opts, int band, int nbands, char* json,
+                                  size_t cap, size_t* needed) {
+  if (!p || nbands < 1 || band < 0 || band >= nbands) return fail(PMG_ERR_ARG, "bad band");
+  PMG_TRY({
+    Plan P;
+    P.pipe = effective(p->p, pvec(params, nparams), opts);
+    P.A = analyze(*P.pipe, pvec(params, nparams));
+    pmg_gpu_spec S;
+    pmg_weights W;
+    spec_or_default(spec, w, S, W);
+    pmg_sched_opts o;
+    if (opts) o = *opts;
+    else pmg_sched_opts_default(&o);
+    std::vector<double> tpi = map_time_per_iter(*p->p, *P.pipe, o.time_per_iter);
+    if (o.time_per_iter) o.time_per_iter = tpi.data();
+    P.sch = schedule(P.A, S, W, o, nullptr);
+    layout_workspace(P);
+    return put_json(xchg_json(P, band, nbands), json, cap, needed);
+  })
+}
+
+pmg_status pmg_run_band_groups(pmg_plan plan, int band, int nbands, int group_begin, int group_end, const pmg_buf* in,
+                               int nin, const pmg_buf* out, int nout, void* workspace, void* stream) {
+  if (!plan || !in || !out || nbands < 1 || band < 0 || band >= nbands || group_begin < 0 || group_end < group_begin)
+    return fail(PMG_ERR_ARG, "bad argument");
+  PMG_TRY({
+    const int gr[2] = {group_begin, group_end};
+    plan_run(*plan->plan, in, nin, out, nout, workspace, (CUstream)stream, band, nbands, 1, nullptr, nullptr, gr);
+    return PMG_OK;
+  })
+}
+
 pmg_status pmg_run_band(pmg_plan plan, int band, int nbands, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
                         void* workspace, void* stream) {
   if (!plan || !in || !out || nbands < 1 || band < 0 || band >= nbands) return fail(PMG_ERR_ARG, "bad argument");

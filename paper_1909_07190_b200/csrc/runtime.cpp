@@ -303,6 +303,29 @@ std::vector<double> profile_groups_us(Plan& P) {
   return us;
 }
 
+void layout_workspace(Plan& P) {
+  // workspace: every materialised stage that is not a liveout
+  const Pipeline& pp = *P.pipe;
+  size_t off = 0;
+  P.ws.clear();
+  for (auto& g : P.sch.groups)
+    for (auto& s : g.gs) {
+      if (!s.materialize) continue;
+      if (std::find(pp.liveouts.begin(), pp.liveouts.end(), s.id) != pp.liveouts.end()) continue;
+      const Ext3& e = P.A.stage_ext[s.id];
+      WsTensor t;
+      t.stage = s.id;
+      t.row_pitch = round_up64(e.e[2] * dtype_size(pp.stages[s.id].dtype), 128);
+      t.rows = e.e[1];
+      t.planes = e.e[0];
+      t.plane_pitch = t.row_pitch * t.rows;
+      t.offset = off;
+      off += (size_t)round_up64(t.plane_pitch * t.planes, 256);
+      P.ws.push_back(t);
+    }
+  P.ws_bytes = off;
+}
+
 std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector<int64_t>& params, int device,
                                   const pmg_gpu_spec* spec, const pmg_weights* w, const pmg_sched_opts* opts) {
   Drv& D = drv();
@@ -370,13 +393,18 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
       const int vx[3][2] = {{1, 4}, {2, 2}, {4, 1}};
       std::unique_ptr<Plan> cbest;
       double ct = tb;
+      // (plus a 6-deep TMA ring for 4-column lanes: Harris in reassociation mode issues fewer instructions per
+      // row and waits on the ring at 4 rows in flight, profiles/harris_sweep_r02c.txt)
       for (auto& q : vx)
-        for (int th : {16, 24, 32, 48, 64, 96, 100, 112, 128}) {
+        for (int th : {16, 24, 32, 48, 64, 96, 100, 112, 128})
+          for (int pf : {4, 6}) {
+          if (pf != 4 && (q[0] != 4 || th < 48)) continue;
           pmg_sched_opts oc = o0;
           oc.group_of_stage = one.data();
           oc.vec = q[0];
           oc.chunks = q[1];
           oc.rows = th;
+          oc.prefetch = pf;
           std::unique_ptr<Plan> Q;
           try {
             Q = plan_create(p, params, device, spec, w, &oc);
@@ -384,7 +412,8 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
             continue;
           }
           double t = time_plan_us(*Q, opts->bands);
-          js << ",{\"round\":\"config\",\"V\":" << q[0] << ",\"TX\":" << q[1] << ",\"TH\":" << th << ",\"us\":" << t << "}";
+          js << ",{\"round\":\"config\",\"V\":" << q[0] << ",\"TX\":" << q[1] << ",\"TH\":" << th << ",\"PREF\":" << pf
+             << ",\"us\":" << t << "}";
           ++pos;
           if (t < ct) { ct = t; cbest = std::move(Q); chosen = pos; }
         }
@@ -433,24 +462,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   P->nimages = (int)pp.images.size();
   P->ntables = (int)pp.tables.size();
   P->nout = (int)pp.liveouts.size();
-  // workspace: every materialised stage that is not a liveout
-  size_t off = 0;
-  for (auto& g : P->sch.groups)
-    for (auto& s : g.gs) {
-      if (!s.materialize) continue;
-      if (std::find(pp.liveouts.begin(), pp.liveouts.end(), s.id) != pp.liveouts.end()) continue;
-      const Ext3& e = P->A.stage_ext[s.id];
-      WsTensor t;
-      t.stage = s.id;
-      t.row_pitch = round_up64(e.e[2] * dtype_size(pp.stages[s.id].dtype), 128);
-      t.rows = e.e[1];
-      t.planes = e.e[0];
-      t.plane_pitch = t.row_pitch * t.rows;
-      t.offset = off;
-      off += (size_t)round_up64(t.plane_pitch * t.planes, 256);
-      P->ws.push_back(t);
-    }
-  P->ws_bytes = off;
+  layout_workspace(*P);
   // compile + load
   std::ostringstream js;
   js << "{\"inlined\":[";
@@ -657,6 +669,55 @@ BandRows band_rows(const Plan& P, int band, int nbands) {
   return b;
 }
 
+BandXchg band_xchg(const Plan& P, int band, int nbands) {
+  const Pipeline& p = *P.pipe;
+  const Analysis& A = P.A;
+  auto hull = [](RowIv& a, RowIv b) {
+    if (b.hi <= b.lo) return;
+    if (a.hi <= a.lo) a = b;
+    else { a.lo = std::min(a.lo, b.lo); a.hi = std::max(a.hi, b.hi); }
+  };
+  const size_t ng = P.sch.groups.size();
+  std::vector<int> group_of(p.stages.size(), -1);
+  for (size_t gi = 0; gi < ng; ++gi)
+    for (int s : P.sch.groups[gi].stages) group_of[s] = (int)gi;
+  BandXchg X;
+  X.own.resize(ng);
+  X.buf.assign(p.stages.size(), RowIv{0, 0});
+  X.need.assign(p.stages.size(), RowIv{0, 0});
+  BandRows br = band_rows(P, band, nbands);
+  X.out = RowIv{br.out_r0, br.out_r1};
+  for (size_t gi = 0; gi < ng; ++gi) {
+    const Group& g = P.sch.groups[gi];
+    const int64_t Hg = g.ext.e[1];
+    X.own[gi] = RowIv{band * Hg / nbands, (band + 1) * Hg / nbands};
+    // rows of the group's own stages: its materialised stages' own rows, then in-group halos (computed inside
+    // the tiles) back-propagated in topological order; reads of other groups' stages and of images are needs
+    std::vector<RowIv> rows(p.stages.size(), RowIv{0, 0});
+    for (auto& s : g.gs)
+      if (s.materialize) rows[s.id] = X.own[gi];
+    for (auto it = g.stages.rbegin(); it != g.stages.rend(); ++it) {
+      const int c = *it;
+      if (rows[c].hi <= rows[c].lo) continue;
+      for (int ri : A.reads_of[c]) {
+        const ReadSite& r = A.reads[ri];
+        const int64_t srows = r.src_is_stage ? A.stage_ext[r.src].e[1] : A.image_ext[r.src].e[1];
+        RowIv nd = rows_needed(A, r, rows[c], srows);
+        if (!r.src_is_stage) hull(X.in, nd);
+        else if (group_of[r.src] == (int)gi) hull(rows[r.src], nd);
+        else hull(X.need[r.src], nd);
+      }
+    }
+  }
+  for (size_t gi = 0; gi < ng; ++gi)
+    for (auto& s : P.sch.groups[gi].gs)
+      if (s.materialize) {
+        X.buf[s.id] = X.own[gi];
+        hull(X.buf[s.id], X.need[s.id]);
+      }
+  return X;
+}
+
 // ------------------------------------------------------------------------------------------ launch
 #pragma pack(push, 1)
 struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, nrows, H, W, pad0, pad1; };
@@ -664,7 +725,7 @@ struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, nrows, H
 static_assert(sizeof(HostTensor) == 56, "PmgTensor mirror");
 
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* ws, CUstream s, int band,
-              int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs) {
+              int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs, const int* groups) {
   std::lock_guard<std::recursive_mutex> lock(P.run_mu);
   Drv& D = drv();
   if (!D.ok) throw Error(-6, D.err);
@@ -701,7 +762,16 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
         if (std::find(p.liveouts.begin(), p.liveouts.end(), st.id) != p.liveouts.end() && !p.consumers[st.id].empty())
           throw Error(-3, "band mode: a liveout that is also consumed by the pipeline is not supported");
   }
-  int64_t in_row_base = banded ? band_rows(P, band, nbands).in_r0 : 0;
+  // halo-exchange band mode: own rows per group, workspace slots holding own + received rows
+  const bool xmode = banded && groups != nullptr;
+  BandXchg X;
+  if (xmode) {
+    X = band_xchg(P, band, nbands);
+    for (size_t si = 0; si < p.stages.size(); ++si) need.stage[si] = X.buf[si];
+    for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) need.group[gi] = X.own[gi];
+  }
+  int64_t in_row_base = xmode ? X.in.lo : banded ? band_rows(P, band, nbands).in_r0 : 0;
+  const int64_t in_row_end = xmode ? X.in.hi : banded ? band_rows(P, band, nbands).in_r1 : 0;
   const bool lanes = P.nlanes > 1;
   std::vector<int> last_on_lane(P.nlanes, -1);
   if (lanes) {
@@ -710,6 +780,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
   }
   for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) {
     if (P.only_group >= 0 && (int)gi != P.only_group) continue;
+    if (xmode && ((int)gi < groups[0] || (int)gi >= groups[1])) continue;
     const Group& g = P.sch.groups[gi];
     Kernel& K = P.kernels[gi];
     const int lane = lanes ? P.lane_of[gi] : 0;
@@ -739,7 +810,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
         t.pp = in[id].plane_pitch_bytes;
         t.fs = in_fs ? in_fs[id] : 0;
         t.row_base = (int32_t)(banded ? in_row_base : 0);
-        t.nrows = (int32_t)(banded ? band_rows(P, band, nbands).in_r1 - in_row_base : A.image_ext[id].e[1]);
+        t.nrows = (int32_t)(banded ? in_row_end - in_row_base : A.image_ext[id].e[1]);
       } else {
         auto lit = std::find(p.liveouts.begin(), p.liveouts.end(), id);
         if (lit != p.liveouts.end()) {

@@ -88,9 +88,25 @@ void plan_destroy(Plan* plan);
 struct BandRows { int64_t out_r0, out_r1, in_r0, in_r1; };
 BandRows band_rows(const Plan& P, int band, int nbands);
 
-// launch every group kernel; band < 0: full image; nframes >= 1 (batch)
+// halo-exchange band geometry: band b computes only its OWN rows of every group,
+// own_g(b) = [b*Hg/n, (b+1)*Hg/n) at the group's row extent Hg, and receives the rows of earlier groups'
+// stages its group needs beyond them from the bands that own them, instead of recomputing the cumulative halo.
+struct BandXchg {
+  std::vector<RowIv> own;    // per group
+  std::vector<RowIv> buf;    // per stage: rows the band's workspace slot holds (own rows + received halo rows)
+  std::vector<RowIv> need;   // per stage: rows the band's later groups read (hull over its reader groups)
+  RowIv in, out;             // image rows of the band's input buffers; liveout rows
+};
+BandXchg band_xchg(const Plan& P, int band, int nbands);
+
+// workspace placement of every materialised non-liveout stage (P.ws, P.ws_bytes)
+void layout_workspace(Plan& P);
+
+// launch every group kernel; band < 0: full image; nframes >= 1 (batch).  groups != nullptr: halo-exchange band
+// mode (band >= 0), launch only groups [groups[0], groups[1]) with the BandXchg geometry.
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* workspace, CUstream s,
-              int band, int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs);
+              int band, int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs,
+              const int* groups = nullptr);
 
 // per-group kernel time of one run (each group launched alone on synthetic inputs; CUDA events, best of 3 samples
 // of 10 runs): the TimePerIter microbenchmark of pmg_profile_stages when groups are single stages

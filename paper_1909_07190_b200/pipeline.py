@@ -170,6 +170,12 @@ class Pipeline:
                                          *[C.byref(x) for x in v]))
         return tuple(x.value for x in v)
 
+    def band_exchange(self, params: dict, band: int, nbands: int, spec=None, weights_=None, opts=None) -> dict:
+        """Halo-exchange band geometry (host only): own rows per group, workspace slots, sends / receives."""
+        arr, n = self.param_values(params)
+        return B.call_json(B.lib.pmg_band_exchange_host, self._h, arr, n, _ref(spec), _ref(weights_), _ref(opts),
+                           band, nbands)
+
     def emit(self, params: dict, spec=None, weights_=None, opts=None) -> dict:
         arr, n = self.param_values(params)
         return B.call_json(B.lib.pmg_emit, self._h, arr, n, _ref(spec), _ref(weights_), _ref(opts))
@@ -294,6 +300,18 @@ class Plan:
         v = [C.c_int64() for _ in range(4)]
         B.check(B.lib.pmg_band_rows(self._h, band, nbands, *[C.byref(x) for x in v]))
         return tuple(x.value for x in v)   # out_r0, out_r1, in_r0, in_r1
+
+    def band_exchange(self, band: int, nbands: int) -> dict:
+        """Halo-exchange band geometry of this plan (pmg_band_exchange)."""
+        return B.call_json(B.lib.pmg_band_exchange, self._h, band, nbands)
+
+    def run_band_groups(self, band: int, nbands: int, g0: int, g1: int, inputs, outputs, workspace, stream=None):
+        """Halo-exchange band mode: groups [g0, g1) of band `band` (inputs hold the geometry's "in" rows)."""
+        ib = (B.Buf * max(1, len(inputs)))(*[_buf(t) for t in inputs])
+        ob = (B.Buf * max(1, len(outputs)))(*[_buf(t) for t in outputs])
+        B.check(B.lib.pmg_run_band_groups(self._h, band, nbands, g0, g1, ib, len(inputs), ob, len(outputs),
+                                          C.c_void_p(workspace.data_ptr()), self._stream(stream)))
+        return outputs
 
     def run_band(self, band: int, nbands: int, inputs, outputs, workspace=None, stream=None):
         """inputs[i] holds image rows [in_r0, in_r1) (tables whole); outputs hold rows [out_r0, out_r1)."""
