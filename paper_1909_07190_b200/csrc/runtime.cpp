@@ -226,8 +226,9 @@ struct CtxGuard {   // make the plan's primary context current for the duration 
 
 static int64_t round_up64(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
 
-// device time of one run of plan Q on synthetic inputs (measured selection, pmg_sched_opts.tune): buffers
-// are allocated here, filled with a constant byte pattern, 2 warm-up runs, then the best of 3 samples of 10 runs
+// device time of one run of plan Q on synthetic inputs (measured selection, pmg_sched_opts.tune): buffer sets
+// (together >= 2x L2, rotated run by run) are allocated here and filled with a constant byte pattern; warm-up
+// runs, then the best of 5 samples of 10 runs per set
 static double time_plan_us(Plan& Q, int nbands = 1) {
   Drv& D = drv();
   const Pipeline& p = *Q.pipe;
@@ -251,35 +252,52 @@ static double time_plan_us(Plan& Q, int nbands = 1) {
     b.ptr = (void*)(uintptr_t)alloc((size_t)(b.plane_pitch_bytes * e.e[0]));
     return b;
   };
-  std::vector<pmg_buf> in, out;
-  for (size_t i = 0; i < p.images.size(); ++i) in.push_back(buf_of(A.image_ext[i], p.images[i].dtype));
-  for (size_t i = 0; i < p.tables.size(); ++i) {
-    pmg_buf b{};
-    b.ptr = (void*)(uintptr_t)alloc((size_t)A.table_len[i] * dtype_size(p.tables[i].dtype));
-    in.push_back(b);
-  }
-  for (int s : p.liveouts) out.push_back(buf_of(A.stage_ext[s], p.stages[s].dtype));
-  void* ws = Q.ws_bytes ? (void*)(uintptr_t)alloc(Q.ws_bytes) : nullptr;
-  // plans made for row bands (sched_opts.bands = n) are timed on the middle band, as one rank runs it: the
-  // buffers point at the band's first input / output row of the full-size allocations
+  // buffer sets rotated between runs, together at least twice the L2 (as bench.py times), at most 4
+  size_t set_bytes = Q.ws_bytes;
+  for (size_t i = 0; i < p.images.size(); ++i)
+    set_bytes += (size_t)(round_up64(A.image_ext[i].e[2] * dtype_size(p.images[i].dtype), 128) * A.image_ext[i].e[1] * A.image_ext[i].e[0]);
+  for (int s : p.liveouts)
+    set_bytes += (size_t)(round_up64(A.stage_ext[s].e[2] * dtype_size(p.stages[s].dtype), 128) * A.stage_ext[s].e[1] * A.stage_ext[s].e[0]);
+  const int nsets = (int)std::min<size_t>(4, std::max<size_t>(1, (2 * (size_t)Q.spec.l2_bytes + set_bytes - 1) / std::max<size_t>(1, set_bytes)));
+  std::vector<std::vector<pmg_buf>> ins(nsets), outs(nsets);
+  std::vector<void*> wss(nsets, nullptr);
   const int band = nbands > 1 ? nbands / 2 : -1;
-  if (band >= 0) {
-    BandRows br = band_rows(Q, band, nbands);
-    for (size_t i = 0; i < p.images.size(); ++i) in[i].ptr = (char*)in[i].ptr + br.in_r0 * in[i].row_pitch_bytes;
-    for (auto& o : out) o.ptr = (char*)o.ptr + br.out_r0 * o.row_pitch_bytes;
+  for (int k = 0; k < nsets; ++k) {
+    auto& in = ins[k];
+    auto& out = outs[k];
+    for (size_t i = 0; i < p.images.size(); ++i) in.push_back(buf_of(A.image_ext[i], p.images[i].dtype));
+    for (size_t i = 0; i < p.tables.size(); ++i) {
+      pmg_buf b{};
+      b.ptr = (void*)(uintptr_t)alloc((size_t)A.table_len[i] * dtype_size(p.tables[i].dtype));
+      in.push_back(b);
+    }
+    for (int s : p.liveouts) out.push_back(buf_of(A.stage_ext[s], p.stages[s].dtype));
+    wss[k] = Q.ws_bytes ? (void*)(uintptr_t)alloc(Q.ws_bytes) : nullptr;
+    // plans made for row bands (sched_opts.bands = n) are timed on the middle band, as one rank runs it: the
+    // buffers point at the band's first input / output row of the full-size allocations
+    if (band >= 0) {
+      BandRows br = band_rows(Q, band, nbands);
+      for (size_t i = 0; i < p.images.size(); ++i) in[i].ptr = (char*)in[i].ptr + br.in_r0 * in[i].row_pitch_bytes;
+      for (auto& o : out) o.ptr = (char*)o.ptr + br.out_r0 * o.row_pitch_bytes;
+    }
   }
+  auto run1 = [&](int r, CUstream st) {
+    const int k = r % nsets;
+    plan_run(Q, ins[k].data(), (int)ins[k].size(), outs[k].data(), (int)outs[k].size(), wss[k], st, band, nbands, 1,
+             nullptr, nullptr);
+  };
   CUstream st;
   check(D.StreamCreate(&st, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
   CUevent e0, e1;
   check(D.EventCreate(&e0, 0), "cuEventCreate");
   check(D.EventCreate(&e1, 0), "cuEventCreate");
-  for (int r = 0; r < 2; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, band, nbands, 1, nullptr, nullptr);
+  for (int r = 0; r < 2 * nsets; ++r) run1(r, st);
   // the paper's statistic: the minimum over samples of the mean of back-to-back runs
-  const int R = 10;
+  const int R = 10 * nsets;
   float ms = 1e30f;
-  for (int sample = 0; sample < 3; ++sample) {
+  for (int sample = 0; sample < 5; ++sample) {
     check(D.EventRecord(e0, st), "cuEventRecord");
-    for (int r = 0; r < R; ++r) plan_run(Q, in.data(), (int)in.size(), out.data(), (int)out.size(), ws, st, band, nbands, 1, nullptr, nullptr);
+    for (int r = 0; r < R; ++r) run1(r, st);
     check(D.EventRecord(e1, st), "cuEventRecord");
     check(D.EventSynchronize(e1), "cuEventSynchronize");
     float m = 0;
@@ -393,12 +411,15 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
       const int vx[3][2] = {{1, 4}, {2, 2}, {4, 1}};
       std::unique_ptr<Plan> cbest;
       double ct = tb;
-      // (plus a 6-deep TMA ring for 4-column lanes: Harris in reassociation mode issues fewer instructions per
-      // row and waits on the ring at 4 rows in flight, profiles/harris_sweep_r02c.txt)
+      // (plus a 6-deep TMA ring for 4-column lanes, with the tile height rounded down so that 6 divides the steps of
+      // a tile and the ring slots resolve at compile time: Harris in reassociation mode issues fewer instructions
+      // per row and waits on the ring at 4 rows in flight, profiles/harris_sweep_r02c.txt)
+      const int t_first = best->sch.groups[0].t_first;
       for (auto& q : vx)
-        for (int th : {16, 24, 32, 48, 64, 96, 100, 112, 128})
+        for (int th0 : {16, 24, 32, 48, 64, 96, 100, 112, 128})
           for (int pf : {4, 6}) {
-          if (pf != 4 && (q[0] != 4 || th < 48)) continue;
+          if (pf != 4 && (q[0] != 4 || th0 < 48)) continue;
+          const int th = pf == 4 ? th0 : th0 - ((th0 - t_first) % pf);   // steps TH - t_first: a multiple of pf
           pmg_sched_opts oc = o0;
           oc.group_of_stage = one.data();
           oc.vec = q[0];

@@ -119,7 +119,7 @@ def test_guard_zones_whole_image_and_bands(name):
     for o, g in zip(plan.outputs, got):
         neq, _ = compare(g, exp[o.name], float_tol=1e-4, rel_range=1e-5 if name == "harris" else None)
         assert neq == 0, f"{name}: {neq} outputs differ from the oracle with guarded inputs"
-    bplan = pmg.Plan(pmg.Pipeline(wl.text), wl.params, opts=pmg.sched_opts(bands=nb))
+    bplan = plan            # the same kernels run the bands (one compile per case)
     for b in range(nb):
         o_r0, o_r1, i_r0, i_r1 = bplan.band_rows(b, nb)
         res = run_guarded(bplan, inp, rows=(i_r0, i_r1), band=(o_r0, o_r1, b, nb))
