@@ -30,6 +30,7 @@ struct Drv {
   CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction);
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
                            void**, void**);
+  CUresult (*LaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**);
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t);
   CUresult (*GetErrorString)(CUresult, const char**);
   CUresult (*MemAlloc)(CUdeviceptr*, size_t);
@@ -79,6 +80,7 @@ inline Drv& drv() {
     PMG_SYM(FuncSetAttribute, "cuFuncSetAttribute");
     PMG_SYM(FuncGetAttribute, "cuFuncGetAttribute");
     PMG_SYM(LaunchKernel, "cuLaunchKernel");
+    PMG_SYM(LaunchKernelEx, "cuLaunchKernelEx");
     PMG_SYM(OccupancyMaxActiveBlocksPerMultiprocessor, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     PMG_SYM(GetErrorString, "cuGetErrorString");
     PMG_SYM(MemAlloc, "cuMemAlloc_v2");

@@ -659,10 +659,18 @@ struct Emitter {
   int phase_of(int t) const { return (((t - g.t_first) % Uk) + Uk) % Uk; }
 
   std::string run() {
-    const KConfig& k = g.cfg;
     o << "// generated by libpmg (emit.cpp) for group " << g.name << ": ";
     for (auto& s : g.gs) o << p.stages[s.id].name << " ";
     o << "\n#include \"pmg_otpw.cuh\"\n\n";
+    header();
+    kernel(true);
+    if (g.xedge && !xe_skip) kernel(true, true);
+    return o.str();
+  }
+
+  // macros, argument struct and tile decoders of the group
+  void header() {
+    const KConfig& k = g.cfg;
     for (auto& P : g.gs) himax = std::max(himax, P.hi);
     for (auto& S : g.streams) himax = std::max(himax, S.hi);
     for (auto& S : g.streams)
@@ -699,9 +707,6 @@ struct Emitter {
          "  const int side = a.ntx - (a.txB - a.txA), h = a.tyB - a.tyA;\n"
          "  const int j = t % side; int r = t / side; ty = a.tyA + r % h; r /= h; pc = r % a.npl; fr = r / a.npl;\n"
          "  tx = j < a.txA ? j : a.txB + (j - a.txA);\n}\n\n";
-    kernel(true);
-    if (g.xedge && !xe_skip) kernel(true, true);
-    return o.str();
   }
   // the interior-tile kernel alone (the selector's register probe reads its ptxas count)
   std::string run_interior_only() {
@@ -782,6 +787,10 @@ struct Emitter {
       o << "  if (gw >= a.ntiles) return;\n"
            "  const int my_tiles = (a.ntiles - gw + nwt - 1) / nwt;\n";
     }
+    // programmatic dependent launch: let the next kernel on the stream be scheduled now, and wait until the
+    // previous one has completed and its writes are visible before the first global access
+    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n"
+         "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
     const bool hs = !g.streams.empty();
     if (hs) {
       // ---- TMA producer state: one request per step, PREF steps ahead of the consumer; lane 0 issues ----

@@ -745,6 +745,80 @@ struct HostTensor { uint64_t ptr; int64_t rp, pp, fs; int32_t row_base, nrows, H
 #pragma pack(pop)
 static_assert(sizeof(HostTensor) == 56, "PmgTensor mirror");
 
+// launch geometry of group gi over rows [gy0, gy1): interior rectangle, x-edge and border tile counts
+struct GroupGeom {
+  int64_t n_int = 0, n_edge = 0, n_bdr = 0, nty_i = 0, nty_b = 0, tyA_b = 0, tyB_b = 0, txA = 0, txB = 0, bxA = 0,
+          bxB = 0, gy0_i = 0;
+  int32_t ylast = INT32_MAX;
+  bool xe = false;
+};
+
+static GroupGeom group_geom(const Plan& P, size_t gi, int64_t gy0, int64_t gy1, int nframes) {
+  const Analysis& A = P.A;
+  const Group& g = P.sch.groups[gi];
+  const Kernel& K = P.kernels[gi];
+  const int64_t Hg = g.ext.e[1], Wg = g.ext.e[2];
+  GroupGeom G;
+  int64_t ntiles = (int64_t)nframes * g.npl * ((gy1 - gy0 + g.cfg.TH - 1) / g.cfg.TH) * g.ntx;
+  if (ntiles > INT32_MAX) throw Error(-3, "too many tiles");
+  // interior rectangle: tiles whose whole wavefront stays inside the image / the computed rows
+  // (matches the emitted bodies: no clamping, no x fix-up, no row checks needed there)
+  int xlm = 0, xrm = 0, himax = 0;
+  for (auto& st : g.streams) {
+    if (st.sx == 0) { xlm = std::max(xlm, st.xl); xrm = std::max(xrm, st.xr); }
+    himax = std::max(himax, st.hi);
+  }
+  for (auto& st : g.gs) himax = std::max(himax, st.hi);
+  auto cdiv = [](int64_t a, int64_t b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
+  auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+  int64_t txA = std::max<int64_t>(0, cdiv(g.PL + xlm, g.OW));
+  int64_t txB = std::min<int64_t>(g.ntx, fdiv(Wg - g.CW - xrm + g.PL, g.OW) + 1);
+  // scaled streams (emit.cpp xb_scaled): the tile's producer row [origin - xl, + row_elems) inside [0, Wp)
+  auto scaled_in = [&](int64_t tx) {
+    const int64_t cx = tx * g.OW - g.PL;
+    for (auto& st : g.streams) {
+      if (st.sx == 0) continue;
+      const Ext3& se = st.src_is_stage ? A.stage_ext[st.src] : A.image_ext[st.src];
+      const int64_t o0 = (st.sx == 1 ? 2 * cx : (cx >= 0 ? cx / 2 : -((-cx + 1) / 2))) - st.xl;
+      if (o0 < 0 || o0 + st.row_elems > se.e[2]) return false;
+    }
+    return true;
+  };
+  while (txA < txB && !scaled_in(txA)) ++txA;
+  while (txB > txA && !scaled_in(txB - 1)) --txB;
+  // interior tile rows: the tiling starts `top` rows below gy0 (a multiple of the border tile height, enough
+  // for the rows the wavefront reads above a tile); its last tile row is shifted up to end at `ylim` (the last
+  // row whose wavefront stays inside the image and the computed rows), overlapping the row before it -- both
+  // compute the same values.  The border kernel takes the rows above the tiling and the TH_b-row tiles from
+  // the one containing ylim down, so only those rows go through the general body.
+  const int THb = g.TH_b > 0 ? g.TH_b : g.cfg.TH;
+  const int64_t top = cdiv(std::max<int64_t>(0, -(int64_t)g.t_first - gy0), THb) * THb;
+  const int64_t ylim = std::min<int64_t>(Hg - himax, gy1);
+  G.gy0_i = gy0 + top;
+  int64_t nty_i = ylim - G.gy0_i >= g.cfg.TH ? cdiv(ylim - G.gy0_i, g.cfg.TH) : 0;
+  if (txB <= txA || nty_i <= 0) { txA = txB = 0; nty_i = 0; }
+  G.nty_i = nty_i;
+  G.txA = txA;
+  G.txB = txB;
+  G.n_int = (int64_t)nframes * g.npl * nty_i * (txB - txA);
+  // x-edge kernel (Group::xedge): the tile columns outside [txA, txB) of the interior tile rows
+  G.xe = K.fn_e && nty_i > 0;
+  G.n_edge = G.xe ? (int64_t)nframes * g.npl * nty_i * (g.ntx - (txB - txA)) : 0;
+  G.bxA = G.xe ? 0 : txA;   // the border kernel's excluded columns
+  G.bxB = G.xe ? g.ntx : txB;
+  G.nty_b = (gy1 - gy0 + THb - 1) / THb;
+  G.tyA_b = nty_i > 0 ? top / THb : 0;
+  G.tyB_b = nty_i > 0 ? (ylim - gy0) / THb : 0;
+  G.n_bdr = (int64_t)nframes * g.npl * (G.nty_b * g.ntx - (G.tyB_b - G.tyA_b) * (G.bxB - G.bxA));
+  G.ylast = nty_i > 0 ? (int32_t)(ylim - g.cfg.TH) : INT32_MAX;
+  return G;
+}
+
+static bool pdl_on() {   // PMG_PDL=0 launches without programmatic dependent launch (experiments)
+  static const bool on = [] { const char* e = getenv("PMG_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout, void* ws, CUstream s, int band,
               int nbands, int nframes, const int64_t* in_fs, const int64_t* out_fs, const int* groups) {
   std::lock_guard<std::recursive_mutex> lock(P.run_mu);
@@ -878,55 +952,11 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
       gy1 = (int32_t)h.hi;
     }
     if (gy1 <= gy0) continue;
-    int64_t nty = (gy1 - gy0 + g.cfg.TH - 1) / g.cfg.TH;
-    int64_t ntiles = (int64_t)nframes * g.npl * nty * g.ntx;
-    if (ntiles > INT32_MAX) throw Error(-3, "too many tiles");
-    // interior rectangle: tiles whose whole wavefront stays inside the image / the computed rows
-    // (matches the emitted bodies: no clamping, no x fix-up, no row checks needed there)
-    int xlm = 0, xrm = 0, himax = 0;
-    for (auto& st : g.streams) {
-      if (st.sx == 0) { xlm = std::max(xlm, st.xl); xrm = std::max(xrm, st.xr); }
-      himax = std::max(himax, st.hi);
-    }
-    for (auto& st : g.gs) himax = std::max(himax, st.hi);
-    auto cdiv = [](int64_t a, int64_t b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
-    auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
-    int64_t txA = std::max<int64_t>(0, cdiv(g.PL + xlm, g.OW));
-    int64_t txB = std::min<int64_t>(g.ntx, fdiv((int64_t)Wg - g.CW - xrm + g.PL, g.OW) + 1);
-    // scaled streams (emit.cpp xb_scaled): the tile's producer row [origin - xl, + row_elems) inside [0, Wp)
-    auto scaled_in = [&](int64_t tx) {
-      const int64_t cx = tx * g.OW - g.PL;
-      for (auto& st : g.streams) {
-        if (st.sx == 0) continue;
-        const Ext3& se = st.src_is_stage ? A.stage_ext[st.src] : A.image_ext[st.src];
-        const int64_t o0 = (st.sx == 1 ? 2 * cx : (cx >= 0 ? cx / 2 : -((-cx + 1) / 2))) - st.xl;
-        if (o0 < 0 || o0 + st.row_elems > se.e[2]) return false;
-      }
-      return true;
-    };
-    while (txA < txB && !scaled_in(txA)) ++txA;
-    while (txB > txA && !scaled_in(txB - 1)) --txB;
-    // interior tile rows: the tiling starts `top` rows below gy0 (a multiple of the border tile height, enough
-    // for the rows the wavefront reads above a tile); its last tile row is shifted up to end at `ylim` (the last
-    // row whose wavefront stays inside the image and the computed rows), overlapping the row before it -- both
-    // compute the same values.  The border kernel takes the rows above the tiling and the TH_b-row tiles from
-    // the one containing ylim down, so only those rows go through the general body.
-    const int THb = g.TH_b > 0 ? g.TH_b : g.cfg.TH;
-    const int64_t top = cdiv(std::max<int64_t>(0, -(int64_t)g.t_first - gy0), THb) * THb;
-    const int64_t ylim = std::min<int64_t>((int64_t)Hg - himax, gy1);
-    const int64_t gy0_i = gy0 + top;
-    int64_t nty_i = ylim - gy0_i >= g.cfg.TH ? cdiv(ylim - gy0_i, g.cfg.TH) : 0;
-    if (txB <= txA || nty_i <= 0) { txA = txB = 0; nty_i = 0; }
-    const int64_t n_int = (int64_t)nframes * g.npl * nty_i * (txB - txA);
-    // x-edge kernel (Group::xedge): the tile columns outside [txA, txB) of the interior tile rows
-    const bool xe = K.fn_e && nty_i > 0;
-    const int64_t n_edge = xe ? (int64_t)nframes * g.npl * nty_i * (g.ntx - (txB - txA)) : 0;
-    const int64_t bxA = xe ? 0 : txA, bxB = xe ? g.ntx : txB;   // the border kernel's excluded columns
-    const int64_t nty_b = (gy1 - gy0 + THb - 1) / THb;
-    const int64_t tyA_b = nty_i > 0 ? top / THb : 0, tyB_b = nty_i > 0 ? (ylim - gy0) / THb : 0;
-    const int64_t n_bdr = (int64_t)nframes * g.npl * (nty_b * g.ntx - (tyB_b - tyA_b) * (bxB - bxA));
-    const int32_t ylast = nty_i > 0 ? (int32_t)(ylim - g.cfg.TH) : INT32_MAX;
-    (void)nty;
+    const GroupGeom G = group_geom(P, gi, gy0, gy1, nframes);
+    const int64_t n_int = G.n_int, n_edge = G.n_edge, n_bdr = G.n_bdr, nty_i = G.nty_i, nty_b = G.nty_b;
+    const int64_t tyA_b = G.tyA_b, tyB_b = G.tyB_b, txA = G.txA, txB = G.txB, bxA = G.bxA, bxB = G.bxB, gy0_i = G.gy0_i;
+    const bool xe = G.xe;
+    const int32_t ylast = G.ylast;
     void* args[] = {buf.data()};
     // diagnosis only (PMG_DIAG_SKIP = "b" / "e" / "i" letters): skip the border / x-edge / interior launches to
     // time the others alone (the output is then incomplete)
@@ -939,7 +969,23 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
                           (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : nty_i), bd ? INT32_MAX : ylast, 0};
       std::memcpy(buf.data() + off_int, ints, 64);
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
-      CUresult r = D.LaunchKernel(f, (unsigned)grid, 1, 1, g.cfg.NW * 32, 1, 1, (unsigned)g.block_smem, st, args, nullptr);
+      // programmatic dependent launch (every emitted kernel starts with griddepcontrol.launch_dependents and
+      // waits with griddepcontrol.wait before its first global access): a kernel that directly follows another
+      // on the stream is launched while its predecessor's last warps still run, hiding the launch latency and
+      // block scheduling of the chain of small kernels (pyramid levels)
+      CUlaunchAttribute attr[1];
+      attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      attr[0].value.programmaticStreamSerializationAllowed = 1;
+      CUlaunchConfig lc{};
+      lc.gridDimX = (unsigned)grid;
+      lc.gridDimY = lc.gridDimZ = 1;
+      lc.blockDimX = g.cfg.NW * 32;
+      lc.blockDimY = lc.blockDimZ = 1;
+      lc.sharedMemBytes = (unsigned)g.block_smem;
+      lc.hStream = st;
+      lc.attrs = attr;
+      lc.numAttrs = pdl_on() ? 1 : 0;
+      CUresult r = D.LaunchKernelEx(&lc, f, args, nullptr);
       if (r != CUDA_SUCCESS) throw Error(-6, std::string("launch of ") + g.name + what + ": " + cu_err(r));
       ++P.last_launches;
     };
@@ -970,7 +1016,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     } else if (n_bdr > 0) {
       launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gs, "_b");
     }
-    (void)ntiles;
+
   }
   if (lanes)   // join every lane back into the caller's stream
     for (int l = 1; l < P.nlanes; ++l)

@@ -76,6 +76,8 @@ HYBRID = [dict(vec=4, chunks=2, smem_chunks=1, rows=16, warps=1, prefetch=4),
 @pytest.mark.parametrize("cfg", HYBRID, ids=lambda c: "V{vec}TX{chunks}S{smem_chunks}TH{rows}".format(**c))
 @pytest.mark.parametrize("name", ["blur", "harris", "unsharp", "camera"])
 def test_hybrid_tiling_parity(name, cfg):
+    if name == "camera" and cfg["chunks"] != 1:
+        pytest.skip("camera: one hybrid configuration (suite time; integer windows in smem follow the same code)")
     """Hybrid tiling (P:645-654): the S leftmost chunks keep their stage windows in shared memory, the rest in
     registers; the result must not change (interior kernel; border tiles stay in registers)."""
     check(name, 1200, 131, opts=pmg.sched_opts(**cfg, tx_size=32))   # wide enough for interior tiles
