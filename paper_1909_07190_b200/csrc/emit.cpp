@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <sstream>
 
@@ -150,8 +151,12 @@ struct Emitter {
       }
       case Expr::ACCESS: return access(e, c);
       case Expr::TABLE: {
-        R idx = toi(ex(*e.args[0], c));
         DType dt = p.tables[e.index].dtype;
+        if (is_const_int(*e.args[0])) {   // loop-invariant lookup: loaded once per kernel (hoisted_tables)
+          const int64_t v = std::min<int64_t>(std::max<int64_t>(eval_int(*e.args[0], A.params), 0), A.table_len[e.index] - 1);
+          return {"tabc" + std::to_string(e.index) + "_" + std::to_string(v), dtype_is_float(dt) ? Kind::Float : Kind::Int};
+        }
+        R idx = toi(ex(*e.args[0], c));
         return {"pmg_ldg<" + std::string(ctype(dt)) + ">(a.tab[" + std::to_string(e.index) + "], pmg_clampi(" + idx.s +
                     ", 0, a.tabn[" + std::to_string(e.index) + "] - 1))",
                 dtype_is_float(dt) ? Kind::Float : Kind::Int};
@@ -569,6 +574,23 @@ struct Emitter {
     return {std::string(f) + "(" + tof(left).s + ", " + b.s + ")", Kind::Float};
   }
 
+  // table lookups at constant indices (the camera's colour matrix after its plane split): one load per kernel
+  // into a register, instead of one per point (same value: the index is clamped to the table as in ex())
+  void hoisted_tables() {
+    std::map<std::pair<int, int64_t>, DType> seen;
+    std::function<void(const Expr&)> scan = [&](const Expr& e) {
+      if (e.op == Expr::TABLE && is_const_int(*e.args[0])) {
+        const int64_t v = std::min<int64_t>(std::max<int64_t>(eval_int(*e.args[0], A.params), 0), A.table_len[e.index] - 1);
+        seen[{e.index, v}] = p.tables[e.index].dtype;
+      }
+      for (auto& a : e.args) scan(*a);
+    };
+    for (auto& P : g.gs) scan(*p.stages[P.id].expr);
+    for (auto& kv : seen)
+      o << "  const " << rtype(kv.second) << " tabc" << kv.first.first << "_" << kv.first.second << " = pmg_ldg<"
+        << ctype(kv.second) << ">(a.tab[" << kv.first.first << "], " << kv.first.second << ");\n";
+  }
+
   // OTPTB ablation (PMG_OTPTB=1): block barriers between stages instead of warp-only synchronisation
   static bool otptb() { const char* e = getenv("PMG_OTPTB"); return e && e[0] == '1'; }
 
@@ -791,6 +813,7 @@ struct Emitter {
     // previous one has completed and its writes are visible before the first global access
     o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n"
          "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    hoisted_tables();
     const bool hs = !g.streams.empty();
     if (hs) {
       // ---- TMA producer state: one request per step, PREF steps ahead of the consumer; lane 0 issues ----

@@ -181,7 +181,7 @@ static double body_ops(const Expr& e) {
       if (e.text == "lerp") return c + 3;
       if (e.text == "clamp") return c + 2;
       return c + 1;
-    case Expr::TABLE: return c + 4;
+    case Expr::TABLE: return is_const_int(*e.args[0]) ? 0.0 : c + 4;   // constant index: hoisted (emit.cpp)
     default: return c;
   }
 }
