@@ -47,6 +47,12 @@ struct Drv {
   CUresult (*EventSynchronize)(CUevent);
   CUresult (*EventElapsedTime)(float*, CUevent, CUevent);
   CUresult (*MemsetD8)(CUdeviceptr, unsigned char, size_t);
+  CUresult (*StreamBeginCapture)(CUstream, CUstreamCaptureMode);
+  CUresult (*StreamEndCapture)(CUstream, CUgraph*);
+  CUresult (*GraphInstantiateWithFlags)(CUgraphExec*, CUgraph, unsigned long long);
+  CUresult (*GraphLaunch)(CUgraphExec, CUstream);
+  CUresult (*GraphExecDestroy)(CUgraphExec);
+  CUresult (*GraphDestroy)(CUgraph);
 };
 
 inline Drv& drv() {
@@ -97,6 +103,12 @@ inline Drv& drv() {
     PMG_SYM(EventSynchronize, "cuEventSynchronize");
     PMG_SYM(EventElapsedTime, "cuEventElapsedTime");
     PMG_SYM(MemsetD8, "cuMemsetD8_v2");
+    PMG_SYM(StreamBeginCapture, "cuStreamBeginCapture_v2");
+    PMG_SYM(StreamEndCapture, "cuStreamEndCapture");
+    PMG_SYM(GraphInstantiateWithFlags, "cuGraphInstantiateWithFlags");
+    PMG_SYM(GraphLaunch, "cuGraphLaunch");
+    PMG_SYM(GraphExecDestroy, "cuGraphExecDestroy");
+    PMG_SYM(GraphDestroy, "cuGraphDestroy");
 #undef PMG_SYM
     if (!all) { d.err = "CUDA driver is missing required symbols"; return; }
     CUresult r = d.Init(0);

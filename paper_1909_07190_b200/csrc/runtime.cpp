@@ -292,12 +292,34 @@ static double time_plan_us(Plan& Q, int nbands = 1) {
   check(D.EventCreate(&e0, 0), "cuEventCreate");
   check(D.EventCreate(&e1, 0), "cuEventCreate");
   for (int r = 0; r < 2 * nsets; ++r) run1(r, st);
-  // the paper's statistic: the minimum over samples of the mean of back-to-back runs
+  // the paper's statistic: the minimum over samples of the mean of back-to-back runs.  The R runs
+  // are captured once into a CUDA graph and replayed, as bench.py times them: host-launched runs of a small
+  // plan would measure the host's enqueue rate (about 10 us per run) instead of the device
   const int R = 10 * nsets;
+  CUgraph graph = nullptr;
+  CUgraphExec exec = nullptr;
+  if (D.StreamBeginCapture(st, CU_STREAM_CAPTURE_MODE_RELAXED) == CUDA_SUCCESS) {
+    bool ok = true;
+    try {
+      for (int r = 0; r < R; ++r) run1(r, st);
+    } catch (const Error&) {
+      ok = false;
+    }
+    if (D.StreamEndCapture(st, &graph) != CUDA_SUCCESS || !ok || !graph ||
+        D.GraphInstantiateWithFlags(&exec, graph, 0) != CUDA_SUCCESS)
+      exec = nullptr;
+  }
+  struct GraphFree {
+    Drv& D; CUgraph& g; CUgraphExec& x;
+    ~GraphFree() { if (x) D.GraphExecDestroy(x); if (g) D.GraphDestroy(g); }
+  } graph_free{D, graph, exec};
+  if (exec) check(D.GraphLaunch(exec, st), "cuGraphLaunch");
   float ms = 1e30f;
   for (int sample = 0; sample < 5; ++sample) {
     check(D.EventRecord(e0, st), "cuEventRecord");
-    for (int r = 0; r < R; ++r) run1(r, st);
+    if (exec) check(D.GraphLaunch(exec, st), "cuGraphLaunch");
+    else
+      for (int r = 0; r < R; ++r) run1(r, st);
     check(D.EventRecord(e1, st), "cuEventRecord");
     check(D.EventSynchronize(e1), "cuEventSynchronize");
     float m = 0;
@@ -814,6 +836,12 @@ static GroupGeom group_geom(const Plan& P, size_t gi, int64_t gy0, int64_t gy1, 
   return G;
 }
 
+// PMG_XMERGE: "1" merged interior + x-edge launches always, "0" never; default: row-band runs only
+static bool xmerge_on(bool banded) {
+  static const int mode = [] { const char* e = getenv("PMG_XMERGE"); return e ? (e[0] == '1' ? 1 : 0) : -1; }();
+  return mode < 0 ? banded : mode == 1;
+}
+
 static bool pdl_on() {   // PMG_PDL=0 launches without programmatic dependent launch (experiments)
   static const bool on = [] { const char* e = getenv("PMG_PDL"); return !(e && e[0] == '0'); }();
   return on;
@@ -883,8 +911,11 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     const CUstream gside = P.lane_side[lane], gside2 = P.lane_side2[lane];
     const CUevent gfork = P.lane_fork[lane], gjoin = P.lane_join[lane], gjoin2 = P.lane_join2[lane];
     if (lanes) {
-      for (int d : P.deps[gi])
-        if (P.lane_of[d] != lane) check(D.StreamWaitEvent(gs, P.ev_group[d], 0), "cuStreamWaitEvent");
+      // (a group timed alone, profile_groups_us, reads what earlier runs left: no producer events to wait on --
+      // they were not recorded in this run, and inside a graph capture they could not be waited on)
+      if (P.only_group < 0)
+        for (int d : P.deps[gi])
+          if (P.lane_of[d] != lane) check(D.StreamWaitEvent(gs, P.ev_group[d], 0), "cuStreamWaitEvent");
       last_on_lane[lane] = (int)gi;
     }
     struct Done {   // every group records its completion event, also when it launches nothing in this run
@@ -961,11 +992,16 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
     // diagnosis only (PMG_DIAG_SKIP = "b" / "e" / "i" letters): skip the border / x-edge / interior launches to
     // time the others alone (the output is then incomplete)
     static const char* skip = getenv("PMG_DIAG_SKIP");
+    // merged interior + x-edge launch: the x-edge body (halo selects at the image's left / right edge) over every
+    // column of the interior tile rows (its decoder walks all columns when txA = txB = 0) -- one launch and no
+    // side stream for them; used for row bands, where a band's launches and their fork / join dominate
+    const bool mrg = xe && n_int > 0 && xmerge_on(banded);
     auto launch = [&](CUfunction f, int bps, int64_t nt, CUstream st, const char* what) {
       const bool bd = f == K.fn_b;
       if (skip && std::strchr(skip, bd ? 'b' : f == K.fn_e ? 'e' : 'i')) return;
       int32_t ints[16] = {Hg, Wg, (int32_t)(bd ? gy0 : gy0_i), gy1, (int32_t)(bd ? nty_b : nty_i), (int32_t)g.ntx,
-                          (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0, (int32_t)(bd ? bxA : txA), (int32_t)(bd ? bxB : txB),
+                          (int32_t)g.npl, (int32_t)nframes, (int32_t)nt, 0, (int32_t)(bd ? bxA : mrg ? 0 : txA),
+                          (int32_t)(bd ? bxB : mrg ? 0 : txB),
                           (int32_t)(bd ? tyA_b : 0), (int32_t)(bd ? tyB_b : nty_i), bd ? INT32_MAX : ylast, 0};
       std::memcpy(buf.data() + off_int, ints, 64);
       int64_t grid = std::min<int64_t>((nt + g.cfg.NW - 1) / g.cfg.NW, (int64_t)bps * P.spec.nsms);
@@ -989,7 +1025,19 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
       if (r != CUDA_SUCCESS) throw Error(-6, std::string("launch of ") + g.name + what + ": " + cu_err(r));
       ++P.last_launches;
     };
-    if (n_int > 0 && (n_bdr > 0 || n_edge > 0)) {
+    if (mrg) {
+      const int64_t n_all = (int64_t)nframes * g.npl * nty_i * g.ntx;
+      if (n_bdr > 0) {
+        check(D.EventRecord(gfork, gs), "cuEventRecord");
+        check(D.StreamWaitEvent(gside, gfork, 0), "cuStreamWaitEvent");
+      }
+      launch(K.fn_e, K.blocks_per_sm_e, n_all, gs, "_e");
+      if (n_bdr > 0) {
+        launch(K.fn_b, K.blocks_per_sm_b, n_bdr, gside, "_b");
+        check(D.EventRecord(gjoin, gside), "cuEventRecord");
+        check(D.StreamWaitEvent(gs, gjoin, 0), "cuStreamWaitEvent");
+      }
+    } else if (n_int > 0 && (n_bdr > 0 || n_edge > 0)) {
       // border / x-edge tiles on the lane's side streams, forked from and joined back into the lane's stream.
       // With an x-edge kernel the border kernel holds only the top / bottom tile rows: the interior kernel is
       // launched first so that its single wave of warps is resident from the start, and the few edge and border
