@@ -137,6 +137,11 @@ typedef struct {
   const double* time_per_iter;  /* NULL = static operation counts; else per stage (declaration order) the measured
                                    TimePerIter in seconds (pmg_profile_stages) used by Alg. 2's
                                    compute term (cost_model 1); stages the schedule rewrote keep the static count */
+  int32_t border_rows;  /* rows of the border-tile kernel's tiles (TH_b, a divisor of TH): <= 0 = 8.  Border tiles
+                           are latency-bound (one warp walks a tile through the general body), so small pyramid
+                           levels and the camera's quad grids run faster with 2-4; measured selection (tune) tries
+                           2, 4 and 8 on its final grouping */
+  int32_t reserved2;
 } pmg_sched_opts;
 
 const char* pmg_last_error(void);

@@ -68,7 +68,8 @@ class SchedOpts(C.Structure):
                 ("smem_chunks", C.c_int32), ("rows", C.c_int32), ("warps", C.c_int32), ("prefetch", C.c_int32),
                 ("tx_size", C.c_int32), ("budget", C.c_int32), ("fuse", C.c_int32), ("regcap", C.c_int32),
                 ("probe", C.c_int32), ("cost_model", C.c_int32), ("bands", C.c_int32), ("no_inline", C.c_int32),
-                ("tune", C.c_int32), ("reassoc", C.c_int32), ("time_per_iter", C.POINTER(C.c_double))]
+                ("tune", C.c_int32), ("reassoc", C.c_int32), ("time_per_iter", C.POINTER(C.c_double)),
+                ("border_rows", C.c_int32), ("reserved2", C.c_int32)]
 
 
 P = C.c_void_p

@@ -267,7 +267,7 @@ bool build_group(const Analysis& A, Group& g, const std::vector<int>& gos) {
   // border kernel's time is one tile's latency; it runs with shorter tiles (measured)
   {
     const char* e = getenv("PMG_BORDER_TH");
-    int want = e ? atoi(e) : 8;
+    int want = e ? atoi(e) : k.THb_want;
     g.TH_b = k.TH;
     for (int d = std::min(want, k.TH); d >= 1; --d)
       if (k.TH % d == 0 && (g.streams.empty() || k.PREF <= d - g.t_first)) { g.TH_b = d; break; }

@@ -28,6 +28,7 @@ struct KConfig {
   int tx_size = 32; // GlMemTxSz choice (32: L2 sector / TMA path; 128: L1 line)
   int regcap = 0;   // registers-per-thread cap via __launch_bounds__ min-blocks (0 = none)
   bool contract = false;   // reassociation mode: f32 a*b+c emitted as one fma (sched_opts.reassoc)
+  int THb_want = 8;        // border-tile rows requested (sched_opts.border_rows); TH_b = the largest divisor of TH <= it
 };
 
 // a read of a group input staged through the TMA ring (unit-stride rows)

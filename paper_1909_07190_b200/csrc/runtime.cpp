@@ -462,6 +462,33 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
         }
       if (cbest) { tb = ct; best = std::move(cbest); }
     }
+    // border-tile rows (TH_b) on the final grouping: border tiles are latency-bound walks of the general body, and
+    // short ones suit small pyramid levels and the camera's quad grids (PMG_BORDER_TH sweep)
+    if (!(grid_env && grid_env[0] == '0') && opts->border_rows <= 0) {
+      keep.push_back(best->sch.group_of_stage);
+      const std::vector<int>& gos = keep.back();
+      const bool one = best->sch.groups.size() == 1;
+      const KConfig bk = best->sch.groups[0].cfg;
+      std::unique_ptr<Plan> bbest;
+      double bt = tb;
+      for (int br : {2, 4}) {
+        pmg_sched_opts oc = o0;
+        oc.group_of_stage = gos.data();
+        oc.border_rows = br;
+        if (one) { oc.vec = bk.V; oc.chunks = bk.TX; oc.rows = bk.TH; oc.prefetch = bk.PREF; }
+        std::unique_ptr<Plan> Q;
+        try {
+          Q = plan_create(p, params, device, spec, w, &oc);
+        } catch (const Error&) {
+          continue;
+        }
+        double t = time_plan_us(*Q, opts->bands);
+        js << ",{\"round\":\"border_rows\",\"TH_b\":" << br << ",\"us\":" << t << "}";
+        ++pos;
+        if (t < bt) { bt = t; bbest = std::move(Q); chosen = pos; }
+      }
+      if (bbest) { tb = bt; best = std::move(bbest); }
+    }
     js << "],\"chosen\":" << chosen << "}";
     best->tune_json = js.str();
     return best;

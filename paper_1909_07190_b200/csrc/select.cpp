@@ -401,7 +401,8 @@ bool best_config(const Analysis& A, Group& g, const std::vector<int>& gos, const
                 if (S_ > TX) continue;
                 Group cand;
                 cand.stages = g.stages;
-                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0, o.reassoc != 0};
+                cand.cfg = KConfig{V, TX, S_, TH, NW, PF, tx, o.regcap > 0 ? o.regcap : 0, o.reassoc != 0,
+                                  o.border_rows > 0 ? o.border_rows : 8};
                 ++count;
                 if (!build_group(A, cand, gos)) { why = cand.why_infeasible; continue; }
                 CostBreakdown c = b200_cost(A, cand, S, w, o.cost_model, o.bands, o.time_per_iter);
@@ -705,7 +706,7 @@ std::string config_json(const Analysis& A, const Group& g) {
   std::ostringstream o;
   o << "{\"name\":\"" << g.name << "\",\"stages\":[";
   for (size_t i = 0; i < g.gs.size(); ++i) o << (i ? "," : "") << "\"" << p.stages[g.gs[i].id].name << "\"";
-  o << "],\"V\":" << k.V << ",\"TX\":" << k.TX << ",\"S\":" << k.S << ",\"TH\":" << k.TH << ",\"NW\":" << k.NW
+  o << "],\"V\":" << k.V << ",\"TX\":" << k.TX << ",\"S\":" << k.S << ",\"TH\":" << k.TH << ",\"TH_b\":" << g.TH_b << ",\"NW\":" << k.NW
     << ",\"PREF\":" << k.PREF << ",\"txSz\":" << k.tx_size << ",\"fracReg\":" << double(k.TX - k.S) / k.TX
     << ",\"tile\":[" << k.V * k.TX << "," << k.TH << ",1],\"block\":[" << 32 * k.NW << ",1,1],\"warp\":[32,1,1]"
     << ",\"CW\":" << g.CW << ",\"OW\":" << g.OW << ",\"PL\":" << g.PL << ",\"PR\":" << g.PR << ",\"t_first\":" << g.t_first

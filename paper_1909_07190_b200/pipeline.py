@@ -43,7 +43,7 @@ def weights(name: str = "b200") -> B.Weights:
 
 def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, warps=-1, prefetch=-1, tx_size=-1,
                budget=0, fuse=True, regcap=0, probe=True, cost_model=0, bands=0, inline=True, tune=False,
-               time_per_iter=None, reassoc=False) -> B.SchedOpts:
+               time_per_iter=None, reassoc=False, border_rows=0) -> B.SchedOpts:
     o = B.SchedOpts()
     B.lib.pmg_sched_opts_default(C.byref(o))
     o.vec, o.chunks, o.smem_chunks, o.rows, o.warps, o.prefetch, o.tx_size = (
@@ -57,6 +57,7 @@ def sched_opts(group_of_stage=None, vec=-1, chunks=-1, smem_chunks=-1, rows=-1, 
     o.no_inline = 0 if inline else 1   # substitute data-expanding stages into their readers
     o.tune = 1 if tune else 0          # measured selection among the DP schedule and its neighbour merges
     o.reassoc = 1 if reassoc else 0    # separable rank-1 stencils + fma contraction (f32 rounding differs)
+    o.border_rows = border_rows        # border-tile rows (TH_b); 0 = automatic
     if time_per_iter is not None:       # measured TimePerIter per stage (Pipeline.profile_stages), Alg. 2 input
         tarr = (C.c_double * len(time_per_iter))(*time_per_iter)
         o._keep_tpi = tarr
