@@ -148,6 +148,54 @@ def cpu_baseline(wl, max_rows=None, parallel=True):
     return out
 
 
+TUNE_CACHE = ROOT / "profiles" / "tuned_schedules.json"
+
+
+def _tune_key(wl, reassoc, bands):
+    import hashlib
+    h = hashlib.sha1(wl.text.encode()).hexdigest()[:12]
+    return f"{wl.name}|{wl.params['W']}x{wl.params['H']}|reassoc={int(bool(reassoc))}|bands={max(0, bands)}|{h}"
+
+
+def tuned_plan(pmg, pipe, wl, dev, reassoc, bands=0, retune=False):
+    """The measured-selection plan (pmg_sched_opts.tune).  Its decision -- the grouping, the border-tile rows and,
+    for one-group plans, the tile -- is stored in profiles/tuned_schedules.json (measured on a B200, keyed by
+    workload, size, arithmetic mode, bands and the pipeline text's hash) and replayed as explicit schedule
+    options, so a bench run does not spend minutes re-timing candidates.  Returns (plan, how)."""
+    cache = json.loads(TUNE_CACHE.read_text()) if TUNE_CACHE.exists() else {}
+    key = _tune_key(wl, reassoc, bands)
+    ent = None if retune else cache.get(key)
+    if ent:
+        o = pmg.sched_opts(group_of_stage=ent["group_of_stage"], border_rows=ent["border_rows"], reassoc=reassoc,
+                           bands=max(0, bands), **ent.get("tile", {}))
+        try:
+            return pmg.Plan(pipe, wl.params, device=dev, opts=o), "measured selection (cached decision, " + TUNE_CACHE.name + ")"
+        except Exception:
+            pass   # a stale entry (pipeline or library changed): measure again
+    plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(tune=True, reassoc=reassoc, bands=max(0, bands)))
+    d = plan.describe()
+    stages = pmg.Pipeline(pipe.rewritten(wl.params, pmg.sched_opts(reassoc=reassoc))["text"]).stages
+    groups = d["schedule"]["groups"]
+    gos = [0] * len(stages)
+    for gi, g in enumerate(groups):
+        for st in g["config"]["stages"]:
+            gos[stages.index(st)] = gi
+    c0 = groups[0]["config"]
+    tune = d.get("tune") or {}
+    cands, chosen = tune.get("candidates", []), tune.get("chosen", 0)
+    pick = cands[chosen] if 0 <= chosen < len(cands) else {}
+    ent = {"group_of_stage": gos, "border_rows": int(pick.get("TH_b", 0)) if pick.get("round") == "border_rows" else 0,
+           "tile": ({"vec": c0["V"], "chunks": c0["TX"], "rows": c0["TH"], "prefetch": c0["PREF"], "warps": c0["NW"]}
+                    if len(groups) == 1 else {}),
+           "us_at_selection": pick.get("us")}
+    cache[key] = ent
+    try:
+        TUNE_CACHE.write_text(json.dumps(cache, indent=1, sort_keys=True))
+    except OSError:
+        pass
+    return plan, "measured selection (timed in this run)"
+
+
 def measure_config(name, dev, steps, warmup, tune=True, reassoc=True):
     """Per-config line (BASELINE.json configs): one plan of the workload at its full size on this GPU, timed like
     the headline (rotating buffer sets >= 2x L2, CUDA graph replay, CUDA events on the launching stream).  C1 blur
@@ -160,10 +208,13 @@ def measure_config(name, dev, steps, warmup, tune=True, reassoc=True):
     W, H = wl.params["W"], wl.params["H"]
     pipe = pmg.Pipeline(wl.text)
     t0 = time.perf_counter()
-    probe = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(reassoc=reassoc))   # the model's schedule
-    # measured selection: merge rounds (for plans of many groups only merges touching the 4 slowest groups), and
-    # the tile grid for one-group plans
-    plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(tune=True, reassoc=reassoc)) if tune else probe
+    # measured selection: merge rounds (for plans of many groups only merges touching the 4 slowest groups), the
+    # tile grid for one-group plans, border-tile rows -- replayed from profiles/tuned_schedules.json when cached
+    if tune:
+        plan, how = tuned_plan(pmg, pipe, wl, dev, reassoc)
+    else:
+        plan, how = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(reassoc=reassoc)), "model"
+    probe = None
     t_plan = time.perf_counter() - t0
     frames = 4096 if name == "blur" else 0
     nfr = max(1, frames)
@@ -233,7 +284,7 @@ def measure_config(name, dev, steps, warmup, tune=True, reassoc=True):
         "alu_frac": ops / (ms * 1e-3) / 1e12 / peak_alu, "algorithmic_ops": ops,
         "groups": len(desc["schedule"]["groups"]), "launches_per_run": plan.last_launches,
         "schedule": ["V%dTX%dTH%d" % (g["config"]["V"], g["config"]["TX"], g["config"]["TH"]) for g in desc["schedule"]["groups"]][:8],
-        "selection": "measured (tune)" if plan is not probe else "model", "plan_s": round(t_plan, 1),
+        "selection": how, "plan_s": round(t_plan, 1),
         "l2": f"{sets} rotating buffer sets", "launch": "CUDA graph replay",
         "arith": "reassoc" if reassoc else "exact", "factored": desc.get("factored", []),
     }
@@ -292,6 +343,8 @@ def main():
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config lines (C1, C3, C4, C5, PB)")
     ap.add_argument("--frames", type=int, default=4096, help="C1 blur: frames in the batch (split across ranks)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) leg (ncu launch lists)")
+    ap.add_argument("--retune", action="store_true",
+                    help="time the measured-selection candidates again instead of replaying profiles/tuned_schedules.json")
     ap.add_argument("--exchange", action="store_true",
                     help="row bands in halo-exchange mode (SURVEY NEXT-2): each band computes its own rows of every "
                          "group and receives halo rows after the producing group (NCCL send/recv at N>1; with "
@@ -332,13 +385,17 @@ def main():
     band = 0 if frames_total else (nb // 2 if nb != world else rank)
     # schedule for this rank's band size; measured selection (tune) among the model's schedule and its neighbours
     reassoc = not args.exact
-    opts = pmg.sched_opts(bands=max(nb, 0), tune=not args.no_tune, reassoc=reassoc)
+    pipe = pmg.Pipeline(wl.text)
+    selection = "model"
     if args.opts:
         kv = dict(x.split("=") for x in args.opts.split(","))
         kv.setdefault("reassoc", int(reassoc))
-        opts = pmg.sched_opts(**{k: int(v) for k, v in kv.items()})
-    pipe = pmg.Pipeline(wl.text)
-    plan = pmg.Plan(pipe, wl.params, device=dev, opts=opts)
+        plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(**{k: int(v) for k, v in kv.items()}))
+        selection = "manual (--opts)"
+    elif args.no_tune:
+        plan = pmg.Plan(pipe, wl.params, device=dev, opts=pmg.sched_opts(bands=max(nb, 0), reassoc=reassoc))
+    else:
+        plan, selection = tuned_plan(pmg, pipe, wl, dev, reassoc, bands=nb if nb > 1 else 0, retune=args.retune)
     desc = plan.describe()
     W, H = wl.params["W"], wl.params["H"]
     inputs_np = wl.inputs()
@@ -589,6 +646,7 @@ def main():
                              "f32 rounding differs from the written order within the north_star tolerance "
                              "(tests/test_gpu_reassoc.py)" % ", ".join(desc.get("factored", [])))
                             if reassoc else "exact: every f32 operation in the written order (bit-identical to the oracle)",
+                   "selection": selection,
                    "schedule": [g["config"] for g in desc["schedule"]["groups"]],
                    "kernels": desc["kernels"]},
         "roofline": ({"bound": "alu", "achieved": alu_achieved, "peak": peak_alu, "unit": "Tops/s",
