@@ -513,11 +513,19 @@ def main():
             step(i)
         torch.cuda.synchronize()
     # (untimed) keep the GPU busy for 0.3 s before the timed region, so that it runs at its working clocks
-    t_w, i = time.perf_counter(), 0
-    while time.perf_counter() - t_w < 0.3:
+    # (the same number of runs on every rank: exchange-mode steps contain point-to-point transfers)
+    t_w = time.perf_counter()
+    for i in range(8):
         step(i)
-        i += 1
-        if i % 64 == 0:
+    torch.cuda.synchronize()
+    n_warm = int(min(20000, 0.3 / max(1e-6, (time.perf_counter() - t_w) / 8)))
+    if world > 1:
+        t = torch.tensor([float(n_warm)], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n_warm = int(t.item())
+    for i in range(n_warm):
+        step(i)
+        if i % 64 == 63:
             torch.cuda.synchronize()
     torch.cuda.synchronize()
     if world > 1:
