@@ -1,4 +1,4 @@
-"""Run one workload a few times (for ncu captures).  python tools/run_once.py harris [opts] [runs]"""
+"""Run one workload a few times (for ncu captures).  python tools/run_once.py harris [opts|auto|cached] [runs]"""
 import sys
 from pathlib import Path
 
@@ -15,8 +15,12 @@ name = sys.argv[1]
 spec = sys.argv[2] if len(sys.argv) > 2 and sys.argv[2] != "auto" else ""
 runs = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 wl = PI.WORKLOADS[name]
-opts = pmg.sched_opts(**{k: int(v) for k, v in (x.split("=") for x in spec.split(","))}) if spec else None
-plan = pmg.Plan(pmg.Pipeline(wl.text), wl.params, opts=opts)
+if spec == "cached":   # the bench's measured-selection decision (profiles/tuned_schedules.json)
+    import bench
+    plan, _ = bench.tuned_plan(pmg, pmg.Pipeline(wl.text), wl, 0, reassoc=True)
+else:
+    opts = pmg.sched_opts(**{k: int(v) for k, v in (x.split("=") for x in spec.split(","))}) if spec else None
+    plan = pmg.Plan(pmg.Pipeline(wl.text), wl.params, opts=opts)
 ins = device_inputs(plan, wl.inputs(), 0)
 outs = plan.alloc_outputs()
 for _ in range(runs):
