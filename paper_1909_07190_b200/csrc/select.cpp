@@ -479,7 +479,18 @@ Schedule schedule(const Analysis& A, const pmg_gpu_spec& S, const pmg_weights& w
     for (int s : p.topo)
       if (std::find(labels.begin(), labels.end(), gos[s]) == labels.end()) labels.push_back(gos[s]);
     std::vector<int> seen;
+    // labels in increasing order when that order is topological (a schedule replayed from its group indices keeps
+    // its group order, and with it the lane assignment); otherwise a topological order of the group DAG
     {
+      std::vector<int> sorted = labels;
+      std::sort(sorted.begin(), sorted.end());
+      bool topo_ok = true;
+      for (int s2 = 0; s2 < n && topo_ok; ++s2)
+        for (int q : p.producers[s2])
+          if (gos[q] > gos[s2]) topo_ok = false;
+      if (topo_ok) seen = sorted;
+    }
+    if (seen.empty()) {
       const size_t L = labels.size();
       auto li = [&](int lab) { return (int)(std::find(labels.begin(), labels.end(), lab) - labels.begin()); };
       std::vector<std::set<int>> preds(L);
