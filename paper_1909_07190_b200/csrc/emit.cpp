@@ -893,8 +893,8 @@ struct Emitter {
       if (!P.materialize) continue;
       std::string T = "a.t[" + std::to_string(P.tensor_slot) + "]";
       o << "    char* obase" << i << " = (char*)" << T << ".ptr + (i64)fr * " << T << ".frame_stride + (i64)pc * " << T
-        << ".plane_pitch - (i64)" << T << ".row_base * " << T << ".row_pitch + (i64)xL * " << dtype_size(p.stages[P.id].dtype)
-        << ";\n";
+        << ".plane_pitch - (i64)" << T << ".row_base * " << T << ".row_pitch + (i64)" << (P.ilv ? "(2 * xL)" : "xL") << " * "
+        << dtype_size(p.stages[P.id].dtype) << ";\n";
     }
     for (int i = 0; i < n; ++i) {
       const GStage& P = g.gs[i];
@@ -1167,7 +1167,8 @@ struct Emitter {
     const GStage& P = g.gs[i];
     DType dt = p.stages[P.id].dtype;
     std::string ct = ctype(dt);
-    int esz = dtype_size(dt);
+    int esz = dtype_size(dt) * (P.ilv ? 2 : 1);   // interleaved: every other element of the liveout row
+    const std::string vst = P.ilv ? "pmg_stg_str2" : "pmg_stg_vec";
     std::string rowv = "row" + std::to_string(i);
     if (fast && tconst) {
       int r = tval + P.hi;
@@ -1191,7 +1192,7 @@ struct Emitter {
         o << "};\n";
         std::string lanes = xe ? " && stk" + std::to_string(kk)
                                : (lo == 0 && hi == 32) ? "" : " && lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi);
-        o << ind << "    pmg_stg_vec_if<" << ct << ", " << V << ">(orow + " << 32 * V * kk * esz << ", w, sp" << lanes << ");\n"
+        o << ind << "    " << vst << "_if<" << ct << ", " << V << ">(orow + " << 32 * V * kk * esz << ", w, sp" << lanes << ");\n"
           << ind << "  }\n";
       }
       o << ind << "}\n";
@@ -1216,17 +1217,17 @@ struct Emitter {
         o << "};\n";
         std::string cond = xe ? "if (stk" + std::to_string(kk) + ") "
                               : (lo == 0 && hi == 32) ? "" : "if (lane >= " + std::to_string(lo) + " && lane < " + std::to_string(hi) + ") ";
-        o << ind << "    " << cond << "pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n" << ind << "  }\n";
+        o << ind << "    " << cond << vst << "<" << ct << ", " << V << ">(" << dst << ", w);\n" << ind << "  }\n";
       } else {
         o << ind << "  {\n" << ind << "    " << ct << " w[" << V << "] = {";
         for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "(" << ct << ")" << sv(i, cur, kk, v);
         o << "};\n";
         o << ind << "    const int xs = xL + " << 32 * V * kk << ";\n"
-          << ind << "    if (xs >= oxlo && xs + V <= oxhi) pmg_stg_vec<" << ct << ", " << V << ">(" << dst << ", w);\n"
+          << ind << "    if (xs >= oxlo && xs + V <= oxhi) " << vst << "<" << ct << ", " << V << ">(" << dst << ", w);\n"
           << ind << "    else if (xs < oxhi && xs + V > oxlo) {\n";
         for (int v = 0; v < V; ++v)
           o << ind << "      if (xs + " << v << " >= oxlo && xs + " << v << " < oxhi) reinterpret_cast<" << ct << "*>(" << dst
-            << ")[" << v << "] = w[" << v << "];\n";
+            << ")[" << (P.ilv ? 2 * v : v) << "] = w[" << v << "];\n";
         o << ind << "    }\n" << ind << "  }\n";
       }
     }

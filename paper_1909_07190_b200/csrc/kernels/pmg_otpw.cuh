@@ -155,6 +155,18 @@ __device__ __forceinline__ void pmg_refill1_elect_nf(u32 bar, u32 total, u32 dst
       ::"r"(bar), "r"(total), "r"(dst), "l"(src), "r"(bytes) : "memory");
 }
 
+// N elements at every other position (stride 2): a quad-resolution phase stored straight into its full-resolution
+// interleaved liveout (runtime.cpp interleave fusion)
+template <typename T, int N>
+__device__ __forceinline__ void pmg_stg_str2(char* dst, const T (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) reinterpret_cast<T*>(dst)[2 * i] = v[i];
+}
+template <typename T, int N>
+__device__ __forceinline__ void pmg_stg_str2_if(char* dst, const T (&v)[N], bool p) {
+  if (p) pmg_stg_str2<T, N>(dst, v);
+}
+
 // predicated vector store (no branch: the interior body stays one basic block)
 template <typename T, int N>
 __device__ __forceinline__ void pmg_stg_vec_if(char* dst, const T (&v)[N], bool p) {

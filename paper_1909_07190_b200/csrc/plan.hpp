@@ -61,6 +61,7 @@ struct GStage {
   bool materialize = false;   // written to global (pipeline liveout or read by a later group)
   bool xfix = false;          // read with dx != 0: replicate out-of-domain columns in border tiles
   bool smem = false;          // hybrid: window kept in shared memory for the S smem chunks
+  bool ilv = false;           // stored at every other column of an interleaved liveout (runtime.cpp interleave fusion)
   int tensor_slot = -1;
   int smem_off = 0;           // per-warp byte offset of its smem window (S > 0)
   int smem_padl = 0;          // elements before column 0 of the smem row (left halo, 16-byte aligned)

@@ -371,6 +371,110 @@ std::vector<double> profile_groups_us(Plan& P) {
   return us;
 }
 
+// integer value of an index / condition expression at (c, y, x) of the stage with `nd` dims (floor / and %)
+static bool ieval(const Expr& e, int nd, const int64_t cyx[3], const std::vector<int64_t>& prm, int64_t& v) {
+  auto fl = [](int64_t a, int64_t b) { int64_t q = a / b; if ((a % b) && ((a < 0) != (b < 0))) --q; return q; };
+  int64_t a = 0, b = 0, c = 0;
+  switch (e.op) {
+    case Expr::INT: v = e.ival; return true;
+    case Expr::PARAM: v = prm.at(e.index); return true;
+    case Expr::VAR: v = cyx[e.index + 3 - nd]; return true;
+    case Expr::BIN:
+      if (!ieval(*e.args[0], nd, cyx, prm, a) || !ieval(*e.args[1], nd, cyx, prm, b)) return false;
+      if (e.text == "+") v = a + b;
+      else if (e.text == "-") v = a - b;
+      else if (e.text == "*") v = a * b;
+      else if (e.text == "/") { if (!b) return false; v = fl(a, b); }
+      else if (e.text == "%") { if (!b) return false; v = a - b * fl(a, b); }
+      else if (e.text == "==") v = a == b;
+      else if (e.text == "!=") v = a != b;
+      else if (e.text == "<") v = a < b;
+      else if (e.text == "<=") v = a <= b;
+      else if (e.text == ">") v = a > b;
+      else if (e.text == ">=") v = a >= b;
+      else return false;
+      return true;
+    case Expr::CALL:
+      if (e.text == "clamp" && e.args.size() == 3) {
+        if (!ieval(*e.args[0], nd, cyx, prm, a) || !ieval(*e.args[1], nd, cyx, prm, b) || !ieval(*e.args[2], nd, cyx, prm, c))
+          return false;
+        v = std::min(std::max(a, b), c);
+        return true;
+      }
+      return false;
+    default: return false;
+  }
+}
+
+// the read a pure select tree picks at (c, y, x): the ACCESS node, or nullptr when the expression is anything else
+static const Expr* pick(const Expr& e, int nd, const int64_t cyx[3], const std::vector<int64_t>& prm) {
+  if (e.op == Expr::ACCESS) return &e;
+  if (e.op == Expr::CALL && e.text == "select" && e.args.size() == 3) {
+    int64_t cond;
+    if (!ieval(*e.args[0], nd, cyx, prm, cond)) return nullptr;
+    return pick(*e.args[cond ? 1 : 2], nd, cyx, prm);
+  }
+  return nullptr;
+}
+
+void detect_interleave(Plan& P) {
+  const char* env = getenv("PMG_ILV");   // "0": keep the interleave as its own kernel
+  P.ilv.clear();
+  P.ilv_skip.assign(P.sch.groups.size(), 0);
+  if (env && env[0] == '0') return;
+  const Pipeline& p = *P.pipe;
+  const Analysis& A = P.A;
+  std::vector<int> group_of(p.stages.size(), -1);
+  for (size_t gi = 0; gi < P.sch.groups.size(); ++gi)
+    for (int s : P.sch.groups[gi].stages) group_of[s] = (int)gi;
+  for (size_t oi = 0; oi < p.liveouts.size(); ++oi) {
+    const int L = p.liveouts[oi];
+    const int gl = group_of[L];
+    if (P.sch.groups[gl].stages.size() != 1 || !p.consumers[L].empty()) continue;
+    const Ext3& le = A.stage_ext[L];
+    if (!le.has[1] || !le.has[2] || le.e[1] % 2 || le.e[2] % 2) continue;
+    const int nd = (int)p.stages[L].vars.size();
+    const int64_t C = le.has[0] ? le.e[0] : 1;
+    std::map<int, Plan::Ilv> found;
+    int gsrc = -1;
+    bool ok = true;
+    for (int64_t c = 0; c < C && ok; ++c)
+      for (int py = 0; py < 2 && ok; ++py)
+        for (int px = 0; px < 2 && ok; ++px) {
+          const Expr* r0 = nullptr;
+          for (int smp = 0; smp < 2 && ok; ++smp) {   // two sample points: the read must be S(y/2, x/2)
+            const int64_t yq = smp ? 3 : 0, xq = smp ? 5 : 0;
+            const int64_t cyx[3] = {c, 2 * yq + py, 2 * xq + px};
+            const Expr* r = pick(*p.stages[L].expr, nd, cyx, A.params);
+            if (!r || !r->is_stage || r->args.size() != 2 || (r0 && r0->index != r->index)) { ok = false; break; }
+            r0 = r;
+            int64_t iy, ix;
+            if (!ieval(*r->args[0], nd, cyx, A.params, iy) || !ieval(*r->args[1], nd, cyx, A.params, ix) || iy != yq ||
+                ix != xq)
+              ok = false;
+          }
+          if (!ok) break;
+          const int S = r0->index;
+          const Ext3& se = A.stage_ext[S];
+          if (found.count(S) || se.has[0] || se.e[1] * 2 != le.e[1] || se.e[2] * 2 != le.e[2] ||
+              p.stages[S].dtype != p.stages[L].dtype || p.consumers[S].size() != 1 || group_of[S] == gl ||
+              (gsrc >= 0 && group_of[S] != gsrc)) {
+            ok = false;
+            break;
+          }
+          gsrc = group_of[S];
+          found[S] = Plan::Ilv{(int)oi, (int)c, py, px};
+        }
+    if (!ok || gsrc < 0) continue;
+    Group& G = P.sch.groups[gsrc];
+    if (G.cfg.S != 0) continue;   // hybrid smem chunks keep their own store path
+    for (auto& st : G.gs)
+      if (found.count(st.id)) st.ilv = true;
+    for (auto& kv : found) P.ilv[kv.first] = kv.second;
+    P.ilv_skip[gl] = 1;
+  }
+}
+
 void layout_workspace(Plan& P) {
   // workspace: every materialised stage that is not a liveout
   const Pipeline& pp = *P.pipe;
@@ -380,6 +484,7 @@ void layout_workspace(Plan& P) {
     for (auto& s : g.gs) {
       if (!s.materialize) continue;
       if (std::find(pp.liveouts.begin(), pp.liveouts.end(), s.id) != pp.liveouts.end()) continue;
+      if (P.ilv.count(s.id)) continue;   // stored into its interleaved liveout
       const Ext3& e = P.A.stage_ext[s.id];
       WsTensor t;
       t.stage = s.id;
@@ -556,6 +661,7 @@ std::unique_ptr<Plan> plan_create(std::shared_ptr<Pipeline> p, const std::vector
   if (o.time_per_iter) o.time_per_iter = tpi.data();
   RegProbe probe = make_probe(P->A);
   P->sch = schedule(P->A, P->spec, P->weights, o, o.probe ? &probe : nullptr);
+  detect_interleave(*P);
   const Pipeline& pp = *p;
   P->nimages = (int)pp.images.size();
   P->ntables = (int)pp.tables.size();
@@ -944,6 +1050,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
   const bool xmode = banded && groups != nullptr;
   BandXchg X;
   if (xmode) {
+    if (!P.ilv.empty()) throw Error(-3, "halo-exchange bands: not supported for a plan with a fused interleave (PMG_ILV=0)");
     X = band_xchg(P, band, nbands);
     for (size_t si = 0; si < p.stages.size(); ++si) need.stage[si] = X.buf[si];
     for (size_t gi = 0; gi < P.sch.groups.size(); ++gi) need.group[gi] = X.own[gi];
@@ -977,6 +1084,7 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
       Drv& D; bool on; CUevent e; CUstream st;
       ~Done() { if (on) D.EventRecord(e, st); }
     } done{D, lanes, lanes ? P.ev_group[gi] : nullptr, gs};
+    if (!P.ilv_skip.empty() && P.ilv_skip[gi]) continue;   // interleave fused into its phases' group
     const int NT = std::max<int>(1, (int)g.tensors.size()), NTAB = std::max(1, P.ntables),
               NP = std::max<int>(1, (int)p.params.size());
     size_t off_tab = sizeof(HostTensor) * (size_t)NT, off_tabn = off_tab + 8 * NTAB, off_prm = off_tabn + 4 * NTAB,
@@ -994,7 +1102,22 @@ void plan_run(Plan& P, const pmg_buf* in, int nin, const pmg_buf* out, int nout,
         t.nrows = (int32_t)(banded ? in_row_end - in_row_base : A.image_ext[id].e[1]);
       } else {
         auto lit = std::find(p.liveouts.begin(), p.liveouts.end(), id);
-        if (lit != p.liveouts.end()) {
+        auto il = P.ilv.find(id);
+        if (il != P.ilv.end()) {
+          // a phase of an interleaved liveout: rows y of the phase are liveout rows 2y+py, columns 2x+px
+          const Plan::Ilv& v = il->second;
+          const pmg_buf& ob = out[v.out];
+          const int64_t ob0 = banded ? r0 : 0, on = banded ? r1 - r0 : A.stage_ext[p.liveouts[v.out]].e[1];
+          const int64_t q0 = (ob0 - v.py + 1) >> 1, q1 = (ob0 + on - v.py + 1) >> 1;   // ceil((r - py) / 2)
+          const int esz = dtype_size(p.stages[id].dtype);
+          t.ptr = (uint64_t)(uintptr_t)((const char*)ob.ptr + (int64_t)v.c * ob.plane_pitch_bytes +
+                                        (2 * q0 + v.py - ob0) * ob.row_pitch_bytes + (int64_t)v.px * esz);
+          t.rp = 2 * ob.row_pitch_bytes;
+          t.pp = ob.plane_pitch_bytes;
+          t.fs = out_fs ? out_fs[v.out] : 0;
+          t.row_base = (int32_t)q0;
+          t.nrows = (int32_t)std::max<int64_t>(0, q1 - q0);
+        } else if (lit != p.liveouts.end()) {
           int oi = int(lit - p.liveouts.begin());
           t.ptr = (uint64_t)(uintptr_t)out[oi].ptr;
           t.rp = out[oi].row_pitch_bytes;

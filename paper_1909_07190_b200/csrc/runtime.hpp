@@ -50,6 +50,11 @@ struct Plan {
   CUcontext ctx = nullptr;
   std::vector<Kernel> kernels;
   std::vector<WsTensor> ws;
+  // interleave fusion: a liveout that only interleaves quad-resolution phases of one group,
+  // L(c, y, x) = S_{c, y%2, x%2}(y/2, x/2), is not launched; the phases store every other element straight into it
+  struct Ilv { int out = -1, c = 0, py = 0, px = 0; };
+  std::map<int, Ilv> ilv;                  // phase stage id -> its place in the liveout
+  std::vector<char> ilv_skip;              // per group: fused away (the interleave's own group)
   size_t ws_bytes = 0;
   int nimages = 0, ntables = 0, nout = 0;
   CUstream side = nullptr;                 // border-tile kernels run here, forked/joined with events
