@@ -251,3 +251,19 @@ def test_multiscale_interp_parity(cfg, W, H):
     got, _ = run_gpu(w.text, w.params, inp, opts=None if cfg is None else pmg.sched_opts(**cfg, tx_size=32))
     neq, _ = compare(got["out"], exp["out"], float_tol=1e-4)
     assert neq == 0
+
+
+def test_camera_interleave_fused(monkeypatch):
+    """Interleave fusion (runtime.cpp detect_interleave): the camera's full-resolution interleave of its quad
+    phases is not launched, the phases store straight into the liveout -- same bytes as the unfused plan and the
+    oracle, two launches fewer."""
+    w = PI.small("camera", 264, 130)
+    inp = w.inputs()
+    exp = evaluate(w.text, w.params, inp)
+    fused, pf = run_gpu(w.text, w.params, inp)
+    n_fused = pf.last_launches
+    monkeypatch.setenv("PMG_ILV", "0")
+    plain, pp = run_gpu(w.text, w.params, inp)
+    for k in exp:
+        assert np.array_equal(fused[k], exp[k]) and np.array_equal(plain[k], exp[k])
+    assert n_fused < pp.last_launches
