@@ -701,6 +701,7 @@ def main():
                       "frac": hbm_achieved / peak_hbm}) | {
                      "traffic": traffic, "peak_source": pk_kind,
                      "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": peak_hbm, "frac": hbm_achieved / peak_hbm,
+                             "frac_8tbs": hbm_achieved / 8000.0,
                              "algorithmic_bytes_per_launch": algo_bytes},
                      "alu": {"achieved_tops": alu_achieved, "peak_tops": peak_alu, "frac": alu_achieved / peak_alu,
                              "algorithmic_ops_per_launch": algo_ops,
