@@ -542,7 +542,7 @@ def main():
     # the runs follow each other on the device with no host or graph launch in between -- the steady state of a
     # stream of images (a graph launch per run costs a few microseconds, comparable to a small plan's run)
     big = None
-    if use_graph and not (xchg and world > 1):
+    if graphs and not (xchg and world > 1):   # (whichever per-run strategy won the warm-up comparison)
         big = torch.cuda.CUDAGraph()
         with torch.cuda.graph(big, stream=cap):
             for i in range(args.steps):
