@@ -685,7 +685,7 @@ def main():
         "config": {"workload": wl.note, "pipeline": wl.pipeline, "W": W, "H": H, "parallelism": f"row-bands x{world}",
                    "launch": ("one CUDA graph of the K timed runs" if big is not None else
                               "CUDA graph replay per buffer set" if use_graph else "host launches") +
-                             (" (faster in warm-up: graph %.4f / host %.4f ms)" % (launch_mode[True], launch_mode[False])
+                             (" (per-run warm-up comparison: graph %.4f / host %.4f ms)" % (launch_mode[True], launch_mode[False])
                               if launch_mode else ""),
                    "l2": f"{sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (>= 2x the {l2 / 1e6:.0f} MB L2)",
                    "arith": ("reassoc: rank-1 stencils evaluated separably (factored: %s) and a*b+c as fma; "
