@@ -1110,8 +1110,11 @@ struct Emitter {
         return g.streams[j].sy == 0 ? "  q_ptr" + std::to_string(j) + " += a.t[" + std::to_string(g.streams[j].tensor_slot) + "].row_pitch;\n"
                                     : std::string();
       };
+      // the proxy fence orders the lanes' generic-proxy reads of this slot before the bulk copy that overwrites it
+      // (PTX memory model).  Dropping it (PMG_FENCE=0, a round-2 experiment) lost 32 elements of a full-size
+      // unsharp run once in many: the reads are usually, not always, complete when the copy lands.
       const char* fe = getenv("PMG_FENCE");
-      const bool fence = fe && fe[0] == '1';
+      const bool fence = !(fe && fe[0] == '0');
       if (g.streams.size() == 1) {
         o << ind << "{\n" << ind << "  " << (fence ? "pmg_refill1_elect" : "pmg_refill1_elect_nf")
           << "(bar0 + 8 * slq, p_total, ring_addr + slq * RING + p_dst0, " << src_of(0)

@@ -142,10 +142,8 @@ __device__ __forceinline__ void pmg_refill1_elect(u32 bar, u32 total, u32 dst, c
       ::"r"(bar), "r"(total), "r"(dst), "l"(src), "r"(bytes) : "memory");
 }
 
-// the same without the proxy fence: the interior main loop refills the slot its lanes read at the start of
-// the step; those LDS reads are issued (in order, through the same MIO path) long before the bulk copy's
-// global fetch can land in shared memory, and the slot's next consumer waits on its mbarrier
-// (DESIGN.md §6 "ring refill"; PMG_FENCE=1 restores the fence)
+// the same without the proxy fence -- experiment only (PMG_FENCE=0): without the fence the lanes' reads of the
+// slot are not ordered before the bulk copy that overwrites it, and a full-size run lost elements once
 __device__ __forceinline__ void pmg_refill1_elect_nf(u32 bar, u32 total, u32 dst, const void* src, u32 bytes) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
